@@ -1,0 +1,178 @@
+/*
+ * sgkkt_b200.h — C ABI of libsgkkt_b200.so, the sm_100a hot path of the
+ * stochastic-Galerkin KKT solver (arXiv 2512.23804, reference package
+ * `sgkkt`).
+ *
+ * Every entry point takes plain device pointers (owned by the caller, e.g.
+ * PyTorch), sizes and a cudaStream_t passed as void*.  Nothing here
+ * allocates device memory, nothing synchronises the host, and every call
+ * returns 0 on success or a negative SGK_E* code (see sgk_last_error()).
+ *
+ * Which reference interface each entry point replaces (paths relative to
+ * /root/reference/pkg/src/sgkkt/):
+ *
+ *   sgk_program_apply      operators.py:88-96   kron_apply
+ *                          operators.py:99-126  kron_apply_sliced
+ *                          preconditioners.py:132-144 HierarchicalGaussSeidel._cross_product
+ *                          preconditioners.py:359-409 CoupledSweepPreconditioner._stiffness_coupling,
+ *                                                     _mass_coupling, _level_rhs
+ *                          operators.py:181-194 steady_kkt_apply
+ *   sgk_trisolve           linalg.py:76-87      LUFactors.solve (SuperLU gstrs),
+ *                          applied to all columns of one degree level at once
+ *                          (preconditioners.py:155-164, 422-433)
+ *   sgk_cheb_step          preconditioners.py:70-98  chebyshev_mass_solve (one step)
+ *   sgk_colscale           preconditioners.py:248-255 (column weights h^gamma, 1/beta)
+ *   sgk_dot_partial,
+ *   sgk_reduce_partials,
+ *   sgk_axpy_dev, ...      krylov.py:78-99,129  fgmres inner products / updates
+ *                          (deterministic two-stage fp64 reductions)
+ *   sgk_f2n / sgk_n2f      operators.py:41-50   matricize / vectorize (layout)
+ */
+#ifndef SGKKT_B200_H
+#define SGKKT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes */
+#define SGK_OK 0
+#define SGK_EINVAL -1   /* bad argument (shape, range, null pointer) */
+#define SGK_ECUDA -2    /* CUDA launch / runtime error */
+#define SGK_ELIMIT -3   /* size beyond a compiled limit */
+
+/* Shared CSR pattern of all spatial matrices (A_t and M share one mesh).
+ * vals holds n_slices value slices in row-block, slice-major order: the
+ * values of row i for slice t are vals[rowptr[i]*n_slices + t*len_i + jj],
+ * len_i = rowptr[i+1]-rowptr[i], jj in [0,len_i).                         */
+typedef struct {
+  int32_t n_rows;
+  int32_t n_slices;
+  const int32_t* rowptr; /* [n_rows+1] */
+  const int32_t* colind; /* [nnz] sorted per row */
+  const double* vals;    /* [nnz*n_slices] */
+} sgk_pattern;
+
+/* Compiled coupling program: out_o[i,k] = alpha_o * sum_e coef_e * U_e[i]
+ * + beta_o * init_o[i,k],  U_(s,l,t)[i] = sum_j A_t[i,j] V_s[j,l].
+ * Built on the host (paper_2512_23804_b200/program.py).                   */
+typedef struct {
+  int32_t n_groups;        /* warp groups of 32 lane items                  */
+  int32_t n_phases;        /* shared-memory phases                           */
+  int32_t n_out_cols;      /* gather targets over all outputs               */
+  int32_t max_phase_slots; /* doubles of shared memory one phase needs      */
+  const int32_t* lane_item;   /* [n_groups*32] (input<<24)|column, -1 idle   */
+  const int32_t* group_step0; /* [n_groups+1] first global step of group    */
+  const int32_t* step_term;   /* [n_steps*32] slice per (step,lane), -1 idle */
+  const int32_t* phase_group0;/* [n_phases+1] first group of phase          */
+  const int32_t* gather_ptr;  /* [n_phases*n_out_cols+1]                    */
+  const int32_t* gather_slot; /* phase-local slot (step-step0)*32+lane      */
+  const double* gather_coef;
+  const int32_t* out_col;     /* [n_out_cols] (output<<24)|column           */
+} sgk_program;
+
+/* Strided view of a node-major (n_rows x ld) fp64 block, columns
+ * [col0, col0+width).                                                       */
+typedef struct {
+  double* ptr;
+  int64_t ld;
+  int32_t col0;
+  int32_t pad;
+} sgk_view;
+
+#define SGK_MAX_IO 4
+
+int sgk_program_apply(const sgk_pattern* pat, const sgk_program* prog,
+                      int32_t n_in, const sgk_view* in,
+                      int32_t n_out, const sgk_view* out,
+                      const sgk_view* init, /* ptr may be NULL per output  */
+                      const double* alpha, const double* beta,
+                      int32_t block_threads, void* stream);
+
+/* Sparse triangular factor (CSR, off-diagonal entries only) with a
+ * dependency-respecting row order (level order).  diag_inv==NULL means
+ * unit diagonal (SuperLU's L).                                              */
+typedef struct {
+  int32_t n;
+  int32_t lower;          /* 1: rows depend on smaller columns (L)         */
+  const int32_t* rowptr;
+  const int32_t* colind;
+  const double* vals;
+  const double* diag_inv; /* [n] or NULL                                   */
+  const int32_t* order;   /* [n] topological (level) order                */
+  int32_t* flags;         /* [n] scratch, zero-initialised once            */
+  int32_t* ticket;        /* [1] scratch                                   */
+} sgk_trifactor;
+
+/* Segmented row view: global row r lives in segment r / seg_rows.          */
+typedef struct {
+  double* ptr[3];
+  int64_t ld;
+  int32_t col0;
+  int32_t seg_rows;
+} sgk_segview;
+
+/* X = Pc U^-1 L^-1 Pr B for `width` columns (linalg.py:83-87).
+ * in_perm[k]  = source row of B for factor row k   (inverse of perm_r)
+ * out_perm[k] = destination row of X for factor row k (inverse of perm_c)
+ * work: n x width contiguous scratch.  B and X may alias.                   */
+int sgk_trisolve(const sgk_trifactor* L, const sgk_trifactor* U,
+                 const int32_t* in_perm, const int32_t* out_perm,
+                 const sgk_segview* b, const sgk_segview* x, double* work,
+                 int32_t width, int32_t epoch, void* stream);
+
+/* One Chebyshev semi-iteration step on all columns (preconditioners.py:89-97):
+ * x_new = omega*(scale .* (b - M x) + x - x_prev) + x_prev,
+ * scale[i] = 1/(alpha*M_ii).  slice selects M inside the shared pattern.    */
+int sgk_cheb_step(const sgk_pattern* pat, int32_t slice, const double* scale,
+                  int64_t n_cols, const double* b, const double* x,
+                  const double* x_prev, double* x_new, double omega,
+                  void* stream);
+
+/* y[i,k] = s * x[i,k] * w[k]  (w may be NULL: y = s*x).                   */
+int sgk_colscale(int64_t n_rows, int64_t n_cols, const double* x,
+                 const double* w, int32_t invert_w, double s, double* y,
+                 void* stream);
+
+/* y = beta*y + mass-stencil(x)*w  etc. are expressed as programs.          */
+
+/* Deterministic fp64 reductions: partials of n-length dot products of x
+ * with each of k vectors y_j = y + j*ystride (k<=SGK_MAX_MDOT), written to
+ * part[j*n_blocks + b]; n_blocks fixed by sgk_reduce_blocks().             */
+#define SGK_MAX_MDOT 8
+int32_t sgk_reduce_blocks(void);
+int sgk_dot_partial(int64_t n, const double* x, const double* y,
+                    int64_t ystride, int32_t k, double* part, void* stream);
+/* out[j] = sum_b part[j*n_blocks+b] in a fixed tree order (+ optional
+ * sqrt when take_sqrt).                                                     */
+int sgk_reduce_partials(const double* part, int32_t k, double* out,
+                        int32_t take_sqrt, void* stream);
+/* y = a*x + b*y with a = sa * (*da if da) and b likewise.                   */
+int sgk_axpby_dev(int64_t n, double sa, const double* da, int32_t inv_a,
+                  const double* x, double sb, const double* db, double* y,
+                  void* stream);
+/* Modified Gram–Schmidt step fused with the next inner product:
+ * w -= h * q_i  (h = *dh), then partial dot of q_next with the new w.        */
+int sgk_mgs_step(int64_t n, const double* dh, const double* q_i, double* w,
+                 const double* q_next, double* part_next, void* stream);
+/* max_j |out[j]| etc. are done on the host from the reduced values.        */
+
+/* Layout: F-order (column k = chaos mode, matricize) <-> node-major.       */
+int sgk_f2n(int64_t n_rows, int64_t n_cols, const double* f, double* nm,
+            void* stream);
+int sgk_n2f(int64_t n_rows, int64_t n_cols, const double* nm, double* f,
+            void* stream);
+
+/* Diagnostics.                                                              */
+const char* sgk_last_error(void);
+int32_t sgk_version(void);
+/* number of kernel launches issued by this library since load (all
+ * entry points; used by bench.py for "gpu_launches").                       */
+int64_t sgk_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,167 @@
+"""ctypes binding of libsgkkt_b200.so (the C ABI declared in include/sgkkt_b200.h).
+
+The product path has no CPU fallback: if the shared library is missing or no
+CUDA device is visible, every device entry point raises ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import torch
+
+__all__ = [
+    "lib",
+    "check",
+    "Pattern",
+    "Program",
+    "View",
+    "TriFactor",
+    "SegView",
+    "stream_ptr",
+    "library_path",
+    "launch_count",
+]
+
+_HERE = Path(__file__).resolve().parent
+_LIBNAME = "libsgkkt_b200.so"
+
+MAX_IO = 4
+MAX_MDOT = 8
+
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+
+
+class Pattern(ctypes.Structure):
+    _fields_ = [
+        ("n_rows", c_i32),
+        ("n_slices", c_i32),
+        ("rowptr", c_vp),
+        ("colind", c_vp),
+        ("vals", c_vp),
+    ]
+
+
+class Program(ctypes.Structure):
+    _fields_ = [
+        ("n_groups", c_i32),
+        ("n_phases", c_i32),
+        ("n_out_cols", c_i32),
+        ("max_phase_slots", c_i32),
+        ("lane_item", c_vp),
+        ("group_step0", c_vp),
+        ("step_term", c_vp),
+        ("phase_group0", c_vp),
+        ("gather_ptr", c_vp),
+        ("gather_slot", c_vp),
+        ("gather_coef", c_vp),
+        ("out_col", c_vp),
+    ]
+
+
+class View(ctypes.Structure):
+    _fields_ = [("ptr", c_vp), ("ld", c_i64), ("col0", c_i32), ("pad", c_i32)]
+
+
+class TriFactor(ctypes.Structure):
+    _fields_ = [
+        ("n", c_i32),
+        ("lower", c_i32),
+        ("rowptr", c_vp),
+        ("colind", c_vp),
+        ("vals", c_vp),
+        ("diag_inv", c_vp),
+        ("order", c_vp),
+        ("flags", c_vp),
+        ("ticket", c_vp),
+    ]
+
+
+class SegView(ctypes.Structure):
+    _fields_ = [("ptr", c_vp * 3), ("ld", c_i64), ("col0", c_i32), ("seg_rows", c_i32)]
+
+
+_SIGNATURES = {
+    "sgk_program_apply": (c_i32, [ctypes.POINTER(Pattern), ctypes.POINTER(Program), c_i32,
+                                  ctypes.POINTER(View), c_i32, ctypes.POINTER(View),
+                                  ctypes.POINTER(View), ctypes.POINTER(c_dbl),
+                                  ctypes.POINTER(c_dbl), c_i32, c_vp]),
+    "sgk_trisolve": (c_i32, [ctypes.POINTER(TriFactor), ctypes.POINTER(TriFactor), c_vp, c_vp,
+                             ctypes.POINTER(SegView), ctypes.POINTER(SegView), c_vp, c_i32,
+                             c_i32, c_vp]),
+    "sgk_cheb_step": (c_i32, [ctypes.POINTER(Pattern), c_i32, c_vp, c_i64, c_vp, c_vp, c_vp,
+                              c_vp, c_dbl, c_vp]),
+    "sgk_colscale": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_i32, c_dbl, c_vp, c_vp]),
+    "sgk_reduce_blocks": (c_i32, []),
+    "sgk_dot_partial": (c_i32, [c_i64, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "sgk_reduce_partials": (c_i32, [c_vp, c_i32, c_vp, c_i32, c_vp]),
+    "sgk_axpby_dev": (c_i32, [c_i64, c_dbl, c_vp, c_i32, c_vp, c_dbl, c_vp, c_vp, c_vp]),
+    "sgk_mgs_step": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "sgk_f2n": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "sgk_n2f": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "sgk_last_error": (ctypes.c_char_p, []),
+    "sgk_version": (c_i32, []),
+    "sgk_launch_count": (c_i64, []),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+
+def library_path() -> Path:
+    return Path(os.environ.get("SGKKT_B200_LIB", str(_HERE / _LIBNAME)))
+
+
+_LIB = None
+
+
+def _load():
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = library_path()
+    if not path.exists():
+        raise RuntimeError(
+            f"{path} is missing: build it with `make` or `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    handle = ctypes.CDLL(str(path))
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = handle
+    return handle
+
+
+def lib():
+    """The loaded library; requires a visible CUDA device (no CPU fallback)."""
+    handle = _load()
+    if not torch.cuda.is_available():
+        raise RuntimeError("libsgkkt_b200 needs a CUDA device; none is visible (no CPU fallback)")
+    return handle
+
+
+def load_without_device():
+    """Load the library for symbol checks only (no compute)."""
+    return _load()
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = _load().sgk_last_error().decode(errors="replace")
+        if rc == -1:
+            raise ValueError(f"{what}: {msg}")
+        raise RuntimeError(f"{what} failed ({rc}): {msg}")
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def launch_count() -> int:
+    return int(_load().sgk_launch_count())

@@ -1,0 +1,184 @@
+// K1/K2/K4 — fused shared-pattern Galerkin "coupling program" kernel.
+//
+// Computes, for every mesh row i,
+//     out_o[i,k] = alpha_o * sum_{(p,h) in G(o,k)} h * U_p[i] + beta_o * init_o[i,k]
+//     U_p[i]     = sum_j A_{t_p}[i,j] * V_{s_p}[j, l_p]
+// where all A_t (and M) share one CSR pattern (t-stacked values) and the
+// list of (t,s,l) products plus the sparse gather G are compiled on the host
+// (program.py).  This single kernel covers
+//   kron_apply          operators.py:88-96   (W = sum_t A_t V H_t)
+//   kron_apply_sliced   operators.py:99-126  (column-range restricted)
+//   HierarchicalGaussSeidel._cross_product  preconditioners.py:132-144
+//   CoupledSweepPreconditioner._level_rhs   preconditioners.py:386-409
+//   steady_kkt_apply    operators.py:181-194 (three block rows in one pass).
+//
+// Work decomposition (B200): one CTA per mesh row at a time (grid-stride over
+// rows, CTAs ordered so rows in flight are adjacent and the 3 grid lines of V
+// they touch stay L2-resident).  Inside a row, each warp owns "groups": 32
+// chaos columns l (one per lane, V rows of the 9 neighbours held in registers)
+// and a list of steps; at a step every lane forms one 9-term stencil dot
+// U_(t,l) with the t the host scheduled for that lane (uniform t across the
+// warp turns the coefficient loads into broadcasts).  U values land in shared
+// memory; after a barrier each thread gathers the sparse H coupling for its
+// output columns from shared memory, accumulating in registers.  Programs
+// larger than the shared-memory budget are split into phases.
+#include "sgk_common.cuh"
+
+namespace sgk {
+
+struct ViewSet {
+  sgk_view v[SGK_MAX_IO];
+};
+struct ScalarSet {
+  double s[SGK_MAX_IO];
+};
+
+constexpr int kChunk = 9;  // stencil entries held in registers per pass
+
+template <int MAXOUT>
+__global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_program prog,
+                                                      ViewSet in, ViewSet out, ViewSet init,
+                                                      ScalarSet alpha, ScalarSet beta) {
+  extern __shared__ double ubuf[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int n_slices = pat.n_slices;
+
+  for (int row = blockIdx.x; row < pat.n_rows; row += gridDim.x) {
+    const int rs = __ldg(pat.rowptr + row);
+    const int len = __ldg(pat.rowptr + row + 1) - rs;
+    const double* arow = pat.vals + (int64_t)rs * n_slices;
+    const int32_t* crow = pat.colind + rs;
+
+    double acc[MAXOUT];
+#pragma unroll
+    for (int r = 0; r < MAXOUT; ++r) acc[r] = 0.0;
+
+    for (int p = 0; p < prog.n_phases; ++p) {
+      const int g0 = __ldg(prog.phase_group0 + p);
+      const int g1 = __ldg(prog.phase_group0 + p + 1);
+      const int qbase = __ldg(prog.group_step0 + g0);
+      for (int g = g0 + warp; g < g1; g += nwarps) {
+        const int item = __ldg(prog.lane_item + g * 32 + lane);
+        const int q0 = __ldg(prog.group_step0 + g);
+        const int q1 = __ldg(prog.group_step0 + g + 1);
+        const double* vb = nullptr;
+        int64_t ldv = 0;
+        if (item >= 0) {
+          const sgk_view& vv = in.v[item >> 24];
+          vb = vv.ptr + vv.col0 + (item & 0xFFFFFF);
+          ldv = vv.ld;
+        }
+        const int passes = len > 0 ? len : 1;
+        for (int c0 = 0; c0 < passes; c0 += kChunk) {
+          const int cl = min(kChunk, len - c0);
+          double v[kChunk];
+#pragma unroll
+          for (int jj = 0; jj < kChunk; ++jj)
+            v[jj] = (vb != nullptr && jj < cl) ? __ldg(vb + (int64_t)__ldg(crow + c0 + jj) * ldv) : 0.0;
+          for (int q = q0; q < q1; ++q) {
+            const int t = __ldg(prog.step_term + q * 32 + lane);
+            if (t >= 0) {
+              const double* at = arow + t * len + c0;
+              double u = 0.0;
+#pragma unroll
+              for (int jj = 0; jj < kChunk; ++jj)
+                if (jj < cl) u = fma(__ldg(at + jj), v[jj], u);
+              const int slot = (q - qbase) * 32 + lane;
+              ubuf[slot] = (c0 == 0) ? u : ubuf[slot] + u;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      const int32_t* gp = prog.gather_ptr + (int64_t)p * prog.n_out_cols;
+#pragma unroll
+      for (int r = 0; r < MAXOUT; ++r) {
+        const int c = threadIdx.x + r * blockDim.x;
+        if (c < prog.n_out_cols) {
+          const int e0 = __ldg(gp + c), e1 = __ldg(gp + c + 1);
+          double a = acc[r];
+          for (int e = e0; e < e1; ++e)
+            a = fma(__ldg(prog.gather_coef + e), ubuf[__ldg(prog.gather_slot + e)], a);
+          acc[r] = a;
+        }
+      }
+      __syncthreads();
+    }
+
+#pragma unroll
+    for (int r = 0; r < MAXOUT; ++r) {
+      const int c = threadIdx.x + r * blockDim.x;
+      if (c < prog.n_out_cols) {
+        const int oc = __ldg(prog.out_col + c);
+        const int o = oc >> 24, k = oc & 0xFFFFFF;
+        double y = alpha.s[o] * acc[r];
+        const sgk_view& iv = init.v[o];
+        if (iv.ptr != nullptr) y += beta.s[o] * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
+        const sgk_view& ov = out.v[o];
+        ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
+      }
+    }
+  }
+}
+
+template <int MAXOUT>
+static int launch_program(const sgk_pattern& pat, const sgk_program& prog, const ViewSet& in,
+                          const ViewSet& out, const ViewSet& init, const ScalarSet& alpha,
+                          const ScalarSet& beta, int threads, cudaStream_t st) {
+  const size_t smem = (size_t)prog.max_phase_slots * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(program_kernel<MAXOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr_set = true;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, program_kernel<MAXOUT>, threads, smem);
+  if (occ < 1) {
+    set_error("program_kernel: zero occupancy (shared memory " + std::to_string(smem) + " B)");
+    return SGK_ELIMIT;
+  }
+  int64_t grid = (int64_t)sm_count() * occ;
+  if (grid > pat.n_rows) grid = pat.n_rows;
+  if (grid < 1) return SGK_OK;
+  program_kernel<MAXOUT><<<(int)grid, threads, smem, st>>>(pat, prog, in, out, init, alpha, beta);
+  return check_launch("program_kernel");
+}
+
+}  // namespace sgk
+
+extern "C" int sgk_program_apply(const sgk_pattern* pat, const sgk_program* prog, int32_t n_in,
+                                 const sgk_view* in, int32_t n_out, const sgk_view* out,
+                                 const sgk_view* init, const double* alpha, const double* beta,
+                                 int32_t block_threads, void* stream) {
+  using namespace sgk;
+  SGK_REQUIRE(pat && prog && out && alpha && beta, "sgk_program_apply: null argument");
+  SGK_REQUIRE(n_in >= 0 && n_in <= SGK_MAX_IO && n_out >= 1 && n_out <= SGK_MAX_IO,
+              "sgk_program_apply: input/output count out of range");
+  SGK_REQUIRE(pat->n_rows >= 0 && pat->n_slices >= 1, "sgk_program_apply: bad pattern");
+  SGK_REQUIRE(prog->n_groups == 0 || n_in >= 1, "sgk_program_apply: program needs inputs");
+  int threads = block_threads > 0 ? block_threads : 256;
+  SGK_REQUIRE(threads % 32 == 0 && threads <= 256, "sgk_program_apply: block_threads must be a multiple of 32, <=256");
+  ViewSet vin{}, vout{}, vinit{};
+  ScalarSet a{}, b{};
+  for (int i = 0; i < n_in; ++i) vin.v[i] = in[i];
+  for (int i = 0; i < n_out; ++i) {
+    vout.v[i] = out[i];
+    SGK_REQUIRE(out[i].ptr != nullptr, "sgk_program_apply: null output");
+    if (init) vinit.v[i] = init[i];
+    a.s[i] = alpha[i];
+    b.s[i] = beta[i];
+  }
+  if (pat->n_rows == 0 || prog->n_out_cols == 0) return SGK_OK;
+  const int per = (prog->n_out_cols + threads - 1) / threads;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (per <= 1) return launch_program<1>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  if (per <= 2) return launch_program<2>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  if (per <= 4) return launch_program<4>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  if (per <= 8) return launch_program<8>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  if (per <= 16) return launch_program<16>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  set_error("sgk_program_apply: too many output columns for one CTA (max 16*block_threads)");
+  return SGK_ELIMIT;
+}

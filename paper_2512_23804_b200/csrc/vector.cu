@@ -1,0 +1,244 @@
+// K5 (Chebyshev step), column scaling, K6 (deterministic Krylov vector ops)
+// and K7 (F-order <-> node-major layout) kernels.
+#include "sgk_common.cuh"
+
+namespace sgk {
+
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 148 * 8;  // fixed => reduction order is fixed
+
+// ---------------------------------------------------------------------------
+// K5: one step of chebyshev_mass_solve (preconditioners.py:89-97) over all
+// columns at once: thread per (row, column); the 9 mass coefficients of the
+// row are broadcast loads, the x rows are coalesced along the columns.
+__global__ void __launch_bounds__(256) cheb_step_kernel(sgk_pattern pat, int slice, const double* __restrict__ scale,
+                                 int64_t n_cols, const double* __restrict__ b,
+                                 const double* __restrict__ x, const double* __restrict__ xp,
+                                 double* __restrict__ xn, double omega) {
+  const int64_t total = (int64_t)pat.n_rows * n_cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n_cols);
+    const int64_t k = idx - (int64_t)i * n_cols;
+    const int rs = __ldg(pat.rowptr + i), len = __ldg(pat.rowptr + i + 1) - rs;
+    const double* a = pat.vals + (int64_t)rs * pat.n_slices + (int64_t)slice * len;
+    double mx = 0.0;
+    for (int jj = 0; jj < len; ++jj) mx = fma(__ldg(a + jj), __ldg(x + (int64_t)__ldg(pat.colind + rs + jj) * n_cols + k), mx);
+    const double resid = __ldg(b + idx) - mx;
+    const double xpv = xp ? __ldg(xp + idx) : 0.0;
+    xn[idx] = omega * (__ldg(scale + i) * resid + __ldg(x + idx) - xpv) + xpv;
+  }
+}
+
+__global__ void colscale_kernel(int64_t n_rows, int64_t n_cols, const double* __restrict__ x,
+                                const double* __restrict__ w, int invert, double s, double* y) {
+  const int64_t total = n_rows * n_cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double v = x[idx];
+    if (w) {
+      const double wk = __ldg(w + idx % n_cols);
+      v = invert ? v / wk : v * wk;
+    }
+    y[idx] = s * v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6: deterministic reductions.  Block b always covers the same index set
+// (grid-stride with a fixed grid) and reduces it in a fixed tree, so the
+// result does not depend on scheduling.
+template <int K>
+__device__ __forceinline__ void block_reduce_store(double (&v)[K], double* part, int nb) {
+  __shared__ double sh[K][kRedThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double s = v[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) sh[j][warp] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double s = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) s += sh[threadIdx.x][w];
+    part[(int64_t)threadIdx.x * nb + blockIdx.x] = s;
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kRedThreads) mdot_kernel(int64_t n, const double* __restrict__ x,
+                                                           const double* __restrict__ y, int64_t ys,
+                                                           double* part) {
+  double v[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) v[j] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)kRedThreads + threadIdx.x; i < n;
+       i += (int64_t)kRedBlocks * kRedThreads) {
+    const double xi = __ldg(x + i);
+#pragma unroll
+    for (int j = 0; j < K; ++j) v[j] = fma(xi, __ldg(y + j * ys + i), v[j]);
+  }
+  block_reduce_store<K>(v, part, kRedBlocks);
+}
+
+__global__ void __launch_bounds__(1024) reduce_partials_kernel(const double* __restrict__ part, double* out,
+                                                               int take_sqrt) {
+  __shared__ double sh[32];
+  const int j = blockIdx.x;
+  const double* p = part + (int64_t)j * kRedBlocks;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < kRedBlocks; b += 1024) s += p[b];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) sh[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 32; ++w) t += sh[w];
+    out[j] = take_sqrt ? sqrt(t) : t;
+  }
+}
+
+__global__ void axpby_kernel(int64_t n, double sa, const double* da, int inv_a, const double* __restrict__ x,
+                             double sb, const double* db, double* y) {
+  double a = sa, b = sb;
+  if (da) a = inv_a ? sa / *da : sa * *da;
+  if (db) b = sb * *db;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double yi = (b == 0.0) ? 0.0 : b * y[i];
+    y[i] = (a == 0.0) ? yi : fma(a, x[i], yi);
+  }
+}
+
+// Modified Gram–Schmidt step (krylov.py:81-84) fused with the partial dot
+// product of the next basis vector against the updated w.
+__global__ void __launch_bounds__(kRedThreads) mgs_step_kernel(int64_t n, const double* dh,
+                                                               const double* __restrict__ q,
+                                                               double* w,
+                                                               const double* __restrict__ qn,
+                                                               double* part) {
+  const double h = *dh;
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)kRedThreads + threadIdx.x; i < n;
+       i += (int64_t)kRedBlocks * kRedThreads) {
+    const double wi = w[i] - h * q[i];
+    w[i] = wi;
+    if (qn) v[0] = fma(__ldg(qn + i), wi, v[0]);
+  }
+  if (qn) block_reduce_store<1>(v, part, kRedBlocks);
+}
+
+// ---------------------------------------------------------------------------
+// K7: layout transposes (32x32 tiles through shared memory).
+__global__ void transpose_kernel(int64_t rows, int64_t cols, const double* __restrict__ in,
+                                 double* __restrict__ out) {
+  // in: rows x cols row-major ; out: cols x rows row-major
+  __shared__ double tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[dy][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t c = c0 + dy, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][dy];
+  }
+}
+
+static int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)sm_count() * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+static int transpose(int64_t rows, int64_t cols, const double* in, double* out, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return SGK_OK;
+  SGK_REQUIRE((cols + 31) / 32 < (1ll << 31) && (rows + 31) / 32 < 65536, "transpose: too large");
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(rows, cols, in, out);
+  return check_launch("transpose_kernel");
+}
+
+}  // namespace sgk
+
+using namespace sgk;
+
+extern "C" int sgk_cheb_step(const sgk_pattern* pat, int32_t slice, const double* scale,
+                             int64_t n_cols, const double* b, const double* x, const double* x_prev,
+                             double* x_new, double omega, void* stream) {
+  SGK_REQUIRE(pat && scale && b && x && x_new, "sgk_cheb_step: null argument");
+  SGK_REQUIRE(slice >= 0 && slice < pat->n_slices, "sgk_cheb_step: slice out of range");
+  SGK_REQUIRE(x_new != x && x_new != x_prev, "sgk_cheb_step: x_new must not alias x/x_prev");
+  const int64_t total = (int64_t)pat->n_rows * n_cols;
+  if (total == 0) return SGK_OK;
+  cheb_step_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(*pat, slice, scale, n_cols, b, x,
+                                                                           x_prev, x_new, omega);
+  return check_launch("cheb_step_kernel");
+}
+
+extern "C" int sgk_colscale(int64_t n_rows, int64_t n_cols, const double* x, const double* w,
+                            int32_t invert_w, double s, double* y, void* stream) {
+  SGK_REQUIRE(x && y, "sgk_colscale: null argument");
+  const int64_t total = n_rows * n_cols;
+  if (total == 0) return SGK_OK;
+  colscale_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(n_rows, n_cols, x, w, invert_w, s, y);
+  return check_launch("colscale_kernel");
+}
+
+extern "C" int32_t sgk_reduce_blocks(void) { return kRedBlocks; }
+
+extern "C" int sgk_dot_partial(int64_t n, const double* x, const double* y, int64_t ystride, int32_t k,
+                               double* part, void* stream) {
+  SGK_REQUIRE(x && y && part, "sgk_dot_partial: null argument");
+  SGK_REQUIRE(k >= 1 && k <= SGK_MAX_MDOT, "sgk_dot_partial: k out of range");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (k) {
+#define SGK_MDOT_CASE(K) \
+  case K:                \
+    mdot_kernel<K><<<kRedBlocks, kRedThreads, 0, st>>>(n, x, y, ystride, part); break;
+    SGK_MDOT_CASE(1) SGK_MDOT_CASE(2) SGK_MDOT_CASE(3) SGK_MDOT_CASE(4)
+    SGK_MDOT_CASE(5) SGK_MDOT_CASE(6) SGK_MDOT_CASE(7) SGK_MDOT_CASE(8)
+#undef SGK_MDOT_CASE
+  }
+  return check_launch("mdot_kernel");
+}
+
+extern "C" int sgk_reduce_partials(const double* part, int32_t k, double* out, int32_t take_sqrt,
+                                   void* stream) {
+  SGK_REQUIRE(part && out && k >= 1, "sgk_reduce_partials: bad argument");
+  reduce_partials_kernel<<<k, 1024, 0, (cudaStream_t)stream>>>(part, out, take_sqrt);
+  return check_launch("reduce_partials_kernel");
+}
+
+extern "C" int sgk_axpby_dev(int64_t n, double sa, const double* da, int32_t inv_a, const double* x,
+                             double sb, const double* db, double* y, void* stream) {
+  SGK_REQUIRE(y && (x || (sa == 0.0 && !da)), "sgk_axpby_dev: null argument");
+  if (n == 0) return SGK_OK;
+  axpby_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, sa, da, inv_a, x, sb, db, y);
+  return check_launch("axpby_kernel");
+}
+
+extern "C" int sgk_mgs_step(int64_t n, const double* dh, const double* q_i, double* w,
+                            const double* q_next, double* part_next, void* stream) {
+  SGK_REQUIRE(dh && q_i && w && (!q_next || part_next), "sgk_mgs_step: null argument");
+  mgs_step_kernel<<<kRedBlocks, kRedThreads, 0, (cudaStream_t)stream>>>(n, dh, q_i, w, q_next, part_next);
+  return check_launch("mgs_step_kernel");
+}
+
+extern "C" int sgk_f2n(int64_t n_rows, int64_t n_cols, const double* f, double* nm, void* stream) {
+  SGK_REQUIRE(f && nm && f != nm, "sgk_f2n: bad argument");
+  // F-order (n_rows x n_cols) is row-major (n_cols x n_rows).
+  return transpose(n_cols, n_rows, f, nm, (cudaStream_t)stream);
+}
+
+extern "C" int sgk_n2f(int64_t n_rows, int64_t n_cols, const double* nm, double* f, void* stream) {
+  SGK_REQUIRE(f && nm && f != nm, "sgk_n2f: bad argument");
+  return transpose(n_rows, n_cols, nm, f, (cudaStream_t)stream);
+}

@@ -1,0 +1,335 @@
+"""Krylov drivers on the B200: drop-in for `sgkkt.krylov` plus the CG and
+MINRES drivers BASELINE.json asks for (the reference has neither,
+SPEC.md:612).
+
+* ``fgmres``  — right-preconditioned flexible GMRES, x0 = 0, no restart,
+  modified Gram–Schmidt with one re-orthogonalisation pass when the
+  remaining component exceeds 1e-8 ||w||, happy-breakdown test
+  ||w|| <= 1e-14 ||w_in||, Givens rotations, stop on |g_{j+1}|/||b|| <= tol
+  (reference krylov.py:45-137).  Vectors live on the device; the
+  (j+2)-vector of Hessenberg entries and the Givens recurrence run on the
+  host exactly as in the reference (one small device->host copy per
+  iteration).
+* ``cg``      — preconditioned conjugate gradients (SPD operator and
+  preconditioner: hGS-CG, configs 1 and 3), stop on the 2-norm relative
+  residual ||r_k|| / ||b||.
+* ``minres``  — preconditioned MINRES (Paige–Saunders / Elman–Silvester–
+  Wathen recurrence) for symmetric indefinite KKT systems with an SPD
+  preconditioner; the 2-norm residual is tracked with the A w recurrence
+  and is the stopping test (SciPy's preconditioned-norm test
+  stops ~3 orders early).
+
+All inner products are deterministic two-stage fp64 reductions (vec.py).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+import torch
+
+from .device import as_device_state, device
+from .vec import Reducer, axpby
+
+__all__ = ["FgmresConfig", "KrylovConfig", "SolveReport", "cg", "fgmres", "minres"]
+
+_REORTH_THRESHOLD = 1e-8
+
+
+@dataclass(frozen=True)
+class FgmresConfig:
+    tol: float
+    max_iters: int = 500
+    record_history: bool = True
+
+    def __post_init__(self):
+        if not 0.0 < self.tol < 1.0:
+            raise ValueError("tolerance must lie in (0, 1)")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be positive")
+
+
+KrylovConfig = FgmresConfig
+
+
+@dataclass
+class SolveReport:
+    iterations: int
+    converged: bool
+    residual_history: np.ndarray
+    wall_time: float
+
+
+def _vec(x) -> tuple[torch.Tensor, bool]:
+    t, host = as_device_state(x)
+    return t.reshape(-1), host
+
+
+def _call(fn: Callable, v: torch.Tensor) -> torch.Tensor:
+    out = fn(v)
+    if not isinstance(out, torch.Tensor) or not out.is_cuda:
+        out, _ = as_device_state(out)
+    out = out.reshape(-1)
+    if out.dtype != torch.float64:
+        raise ValueError("operator returned non-float64 data")
+    return out
+
+
+def _return(x: torch.Tensor, host: bool, like):
+    if not host:
+        return x
+    if isinstance(like, torch.Tensor):
+        return x.to("cpu")
+    return x.cpu().numpy()
+
+
+class _Basis:
+    """Krylov vectors in (8, n) chunks so up to 8 inner products share one
+    pass over w (equal stride for the multi-dot kernel)."""
+
+    def __init__(self, n: int, dev):
+        self.n = n
+        self.dev = dev
+        self.chunks: list[torch.Tensor] = []
+
+    def slot(self, i: int) -> torch.Tensor:
+        while i // 8 >= len(self.chunks):
+            self.chunks.append(torch.empty((8, self.n), dtype=torch.float64, device=self.dev))
+        return self.chunks[i // 8][i % 8]
+
+    def block(self, lo: int, hi: int) -> torch.Tensor:
+        return self.chunks[lo // 8][lo % 8 : lo % 8 + (hi - lo)]
+
+
+def fgmres(apply_op: Callable, apply_prec: Callable | None, b, cfg: FgmresConfig):
+    start = time.perf_counter()
+    bd, host = _vec(b)
+    dev = bd.device
+    n = bd.numel()
+    red = Reducer(dev)
+    scal = torch.zeros(4, dtype=torch.float64, device=dev)
+    b_norm = float(red.norm(bd, scal[0:1]).item())
+    if b_norm == 0.0:
+        raise ValueError("right-hand side must be nonzero")
+    prec = apply_prec if apply_prec is not None else (lambda v: v)
+
+    max_iters = min(cfg.max_iters, n)
+    basis = _Basis(n, dev)
+    directions: list[torch.Tensor] = []
+    hess = np.zeros((max_iters + 1, max_iters))
+    cs = np.zeros(max_iters)
+    sn = np.zeros(max_iters)
+    g = np.zeros(max_iters + 1)
+    g[0] = b_norm
+    axpby(basis.slot(0), bd, 1.0 / b_norm, 0.0)
+    hdev = torch.zeros(max_iters + 2, dtype=torch.float64, device=dev)
+    ddev = torch.zeros(max_iters + 2, dtype=torch.float64, device=dev)
+    history = []
+    converged = False
+    n_iter = 0
+    for j in range(max_iters):
+        n_iter = j + 1
+        z = _call(prec, basis.slot(j))
+        directions.append(z)
+        w = _call(apply_op, z)
+        if w.data_ptr() == z.data_ptr() or any(w.data_ptr() == c.data_ptr() for c in basis.chunks):
+            w = w.clone()
+        # modified Gram–Schmidt (reference krylov.py:81-84), fused dot+update
+        red.norm(w, scal[0:1])  # ||w_in||
+        red.dot(basis.slot(0), w, hdev[0:1])
+        for i in range(j + 1):
+            nxt = basis.slot(i + 1) if i < j else None
+            red.mgs_step(hdev[i : i + 1], basis.slot(i), w, nxt, hdev[i + 1 : i + 2] if nxt is not None else None)
+        red.norm(w, scal[1:2])
+        for lo in range(0, j + 1, 8):
+            hi = min(j + 1, (lo // 8 + 1) * 8)
+            red.dots(w, basis.block(lo, hi), ddev[lo:hi])
+        host_vals = torch.cat([scal[0:2], hdev[: j + 1], ddev[: j + 1]]).cpu().numpy()
+        w_norm_in, w_norm = host_vals[0], host_vals[1]
+        hess[: j + 1, j] = host_vals[2 : 3 + j]
+        defect = np.abs(host_vals[3 + j :]).max() if w_norm > 0 else 0.0
+        if w_norm == 0.0 or defect > _REORTH_THRESHOLD * w_norm:
+            red.dot(basis.slot(0), w, hdev[0:1])
+            for i in range(j + 1):
+                nxt = basis.slot(i + 1) if i < j else None
+                red.mgs_step(hdev[i : i + 1], basis.slot(i), w, nxt, hdev[i + 1 : i + 2] if nxt is not None else None)
+            red.norm(w, scal[1:2])
+            hv = torch.cat([scal[1:2], hdev[: j + 1]]).cpu().numpy()
+            hess[: j + 1, j] += hv[1:]
+            w_norm = hv[0]
+        hess[j + 1, j] = w_norm
+
+        breakdown = w_norm <= 1e-14 * max(w_norm_in, 1e-300)
+        if not breakdown:
+            axpby(basis.slot(j + 1), w, 1.0 / w_norm, 0.0)
+
+        for i in range(j):
+            t1 = cs[i] * hess[i, j] + sn[i] * hess[i + 1, j]
+            t2 = -sn[i] * hess[i, j] + cs[i] * hess[i + 1, j]
+            hess[i, j] = t1
+            hess[i + 1, j] = t2
+        denom = np.hypot(hess[j, j], hess[j + 1, j])
+        if denom == 0.0:
+            cs[j], sn[j] = 1.0, 0.0
+        else:
+            cs[j] = hess[j, j] / denom
+            sn[j] = hess[j + 1, j] / denom
+        hess[j, j] = denom
+        hess[j + 1, j] = 0.0
+        g[j + 1] = -sn[j] * g[j]
+        g[j] = cs[j] * g[j]
+        rel_res = abs(g[j + 1]) / b_norm
+        history.append(rel_res)
+        if rel_res <= cfg.tol or breakdown:
+            converged = True
+            break
+
+    m = n_iter
+    y = np.zeros(m)
+    for i in range(m - 1, -1, -1):
+        y[i] = (g[i] - hess[i, i + 1 : m] @ y[i + 1 : m]) / hess[i, i]
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    for i in range(m):
+        axpby(x, directions[i], float(y[i]), 1.0)
+    report = SolveReport(
+        iterations=m,
+        converged=converged,
+        residual_history=np.array(history) if cfg.record_history else np.array([]),
+        wall_time=time.perf_counter() - start,
+    )
+    return _return(x, host, b), report
+
+
+def cg(apply_op: Callable, apply_prec: Callable | None, b, cfg: FgmresConfig):
+    """Preconditioned CG from x0 = 0; stops when ||r_k||_2 / ||b||_2 <= tol
+    (recurrence residual)."""
+    start = time.perf_counter()
+    bd, host = _vec(b)
+    dev = bd.device
+    n = bd.numel()
+    red = Reducer(dev)
+    sc = torch.zeros(4, dtype=torch.float64, device=dev)
+    b_norm = float(red.norm(bd, sc[0:1]).item())
+    if b_norm == 0.0:
+        raise ValueError("right-hand side must be nonzero")
+    prec = apply_prec if apply_prec is not None else (lambda v: v)
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    r = bd.clone()
+    z = _call(prec, r)
+    p = z.clone()
+    rz = float(red.dot(r, z, sc[1:2]).item())
+    history = []
+    converged = False
+    it = 0
+    max_iters = cfg.max_iters
+    for it in range(1, max_iters + 1):
+        q = _call(apply_op, p)
+        pq = float(red.dot(p, q, sc[2:3]).item())
+        if pq <= 0.0:
+            raise ValueError("operator or preconditioner is not positive definite (p.Ap <= 0)")
+        alpha = rz / pq
+        axpby(x, p, alpha, 1.0)
+        axpby(r, q, -alpha, 1.0)
+        rel = float(red.norm(r, sc[0:1]).item()) / b_norm
+        history.append(rel)
+        if rel <= cfg.tol:
+            converged = True
+            break
+        z = _call(prec, r)
+        rz_new = float(red.dot(r, z, sc[1:2]).item())
+        beta = rz_new / rz
+        rz = rz_new
+        axpby(p, z, 1.0, beta)
+    report = SolveReport(it, converged, np.array(history) if cfg.record_history else np.array([]),
+                         time.perf_counter() - start)
+    return _return(x, host, b), report
+
+
+def minres(apply_op: Callable, apply_prec: Callable | None, b, cfg: FgmresConfig):
+    """Preconditioned MINRES from x0 = 0 for symmetric A and SPD
+    preconditioner P; stops on the true-2-norm relative residual tracked by
+    r_j = r_{j-1} - c_{j+1} eta A w_{j+1}."""
+    start = time.perf_counter()
+    bd, host = _vec(b)
+    dev = bd.device
+    n = bd.numel()
+    red = Reducer(dev)
+    sc = torch.zeros(4, dtype=torch.float64, device=dev)
+    b_norm = float(red.norm(bd, sc[0:1]).item())
+    if b_norm == 0.0:
+        raise ValueError("right-hand side must be nonzero")
+    prec = apply_prec if apply_prec is not None else (lambda v: v)
+    zeros = lambda: torch.zeros(n, dtype=torch.float64, device=dev)
+    x = zeros()
+    r = bd.clone()
+    v_old = zeros()
+    v = bd.clone()
+    z = _call(prec, v)
+    zv = float(red.dot(z, v, sc[1:2]).item())
+    if zv <= 0.0:
+        raise ValueError("preconditioner is not positive definite")
+    gamma = np.sqrt(zv)
+    gamma_old = 1.0
+    eta = gamma
+    s_old = s = 0.0
+    c_old = c = 1.0
+    w_old, w = zeros(), zeros()
+    aw_old, aw = zeros(), zeros()
+    history = []
+    converged = False
+    it = 0
+    max_iters = cfg.max_iters
+    for it in range(1, max_iters + 1):
+        zn = z.clone() if z.data_ptr() in (v.data_ptr(), r.data_ptr()) else z
+        axpby(zn, None, 0.0, 1.0 / gamma)  # z_j /= gamma_j
+        az = _call(apply_op, zn)
+        if az.data_ptr() == zn.data_ptr():
+            az = az.clone()
+        delta = float(red.dot(az, zn, sc[1:2]).item())
+        # v_{j+1} = A z_j - (delta/gamma) v_j - (gamma/gamma_old) v_{j-1}
+        v_new = az.clone()
+        axpby(v_new, v, -delta / gamma, 1.0)
+        axpby(v_new, v_old, -gamma / gamma_old, 1.0)
+        z_new = _call(prec, v_new)
+        zv = float(red.dot(z_new, v_new, sc[2:3]).item())
+        if zv < 0.0:
+            raise ValueError("preconditioner is not positive definite")
+        gamma_new = np.sqrt(zv)
+        a0 = c * delta - c_old * s * gamma
+        a1 = np.sqrt(a0 * a0 + gamma_new * gamma_new)
+        a2 = s * delta + c_old * c * gamma
+        a3 = s_old * gamma
+        c_new = a0 / a1
+        s_new = gamma_new / a1
+        # w_{j+1} = (z_j - a3 w_{j-1} - a2 w_j)/a1 ; same recurrence for A w
+        w_new = zn.clone()
+        axpby(w_new, w_old, -a3, 1.0)
+        axpby(w_new, w, -a2, 1.0)
+        axpby(w_new, None, 0.0, 1.0 / a1)
+        aw_new = az.clone()
+        axpby(aw_new, aw_old, -a3, 1.0)
+        axpby(aw_new, aw, -a2, 1.0)
+        axpby(aw_new, None, 0.0, 1.0 / a1)
+        axpby(x, w_new, c_new * eta, 1.0)
+        axpby(r, aw_new, -c_new * eta, 1.0)
+        eta = -s_new * eta
+        rel = float(red.norm(r, sc[0:1]).item()) / b_norm
+        history.append(rel)
+        v_old, v = v, v_new
+        z = z_new
+        w_old, w = w, w_new
+        aw_old, aw = aw, aw_new
+        gamma_old, gamma = gamma, gamma_new
+        c_old, c = c, c_new
+        s_old, s = s, s_new
+        if rel <= cfg.tol:
+            converged = True
+            break
+        if gamma == 0.0:
+            break
+    report = SolveReport(it, converged, np.array(history) if cfg.record_history else np.array([]),
+                         time.perf_counter() - start)
+    return _return(x, host, b), report

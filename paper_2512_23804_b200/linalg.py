@@ -1,0 +1,230 @@
+"""Sparse LU for the lead-term solves: factor once on the host with SuperLU
+(exactly the reference call, linalg.py:103-120:
+``splu(A.tocsc(), diag_pivot_thresh=1.0)`` with the default COLAMD column
+order), then run every triangular solve on the GPU (csrc/trisolve.cu) for
+all right-hand-side columns of a degree level at once.
+
+SuperLU convention (verified in tests/test_linalg_host.py):
+    Pr A Pc = L U,  Pr[perm_r[i], i] = 1,  Pc[i, perm_c[i]] = 1,
+    x = Pc U^-1 L^-1 Pr b   =>  factor row k reads b[iperm_r[k]] and writes
+    x[iperm_c[k]].
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse as sp
+import scipy.sparse.linalg
+import torch
+from scipy.sparse import csr_matrix
+
+from . import _lib
+from .device import _f64, _i32, as_device_state, device
+
+__all__ = [
+    "LUFactors",
+    "SingularMatrixError",
+    "TriangularFactors",
+    "csr_from_coo",
+    "level_schedule",
+    "lu_solve",
+    "sparse_lu",
+]
+
+
+class SingularMatrixError(np.linalg.LinAlgError):
+    """Raised when a sparse factorization meets a zero pivot (linalg.py:39-40)."""
+
+
+def csr_from_coo(nrows, ncols, rows, cols, vals) -> csr_matrix:
+    """Triplets -> CSR with duplicates summed and sorted columns
+    (reference linalg.py:43-62)."""
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    vals = np.asarray(vals, dtype=np.float64)
+    if rows.size and (rows.min() < 0 or rows.max() >= nrows):
+        raise ValueError("row index out of range")
+    if cols.size and (cols.min() < 0 or cols.max() >= ncols):
+        raise ValueError("column index out of range")
+    mat = sp.coo_matrix((vals, (rows, cols)), shape=(nrows, ncols)).tocsr()
+    mat.sum_duplicates()
+    mat.sort_indices()
+    if not np.all(np.isfinite(mat.data)):
+        raise ValueError("non-finite entries in assembled matrix")
+    return mat
+
+
+def level_schedule(strict: csr_matrix, lower: bool) -> tuple[np.ndarray, int]:
+    """Topological order of the rows of a strictly triangular factor by
+    dependency level, and the number of levels (the critical-path depth)."""
+    n = strict.shape[0]
+    indptr, indices = strict.indptr, strict.indices
+    level = np.zeros(n, dtype=np.int64)
+    rng = range(n) if lower else range(n - 1, -1, -1)
+    for k in rng:
+        a, b = indptr[k], indptr[k + 1]
+        if b > a:
+            level[k] = level[indices[a:b]].max() + 1
+    order = np.argsort(level, kind="stable")
+    if not lower:
+        # inside a level keep descending row order (matches the dependency direction)
+        order = np.lexsort((-np.arange(n), level))
+    depth = int(level.max()) + 1 if n else 0
+    return order.astype(np.int64), depth
+
+
+@dataclass(eq=False)
+class TriangularFactors:
+    """Device copy of one SuperLU factorization."""
+
+    n: int
+    depth_l: int
+    depth_u: int
+    nnz_l: int
+    nnz_u: int
+    bufs: list
+    l_struct: _lib.TriFactor
+    u_struct: _lib.TriFactor
+    in_perm: torch.Tensor
+    out_perm: torch.Tensor
+    epoch: int = 0
+
+    @classmethod
+    def from_superlu(cls, lu) -> "TriangularFactors":
+        n = lu.shape[0]
+        lmat = sp.csr_matrix(lu.L)
+        umat = sp.csr_matrix(lu.U)
+        l_strict = sp.tril(lmat, k=-1, format="csr")
+        u_strict = sp.triu(umat, k=1, format="csr")
+        for m in (l_strict, u_strict):
+            m.sum_duplicates()
+            m.sort_indices()
+        diag = umat.diagonal()
+        ord_l, depth_l = level_schedule(l_strict, lower=True)
+        ord_u, depth_u = level_schedule(u_strict, lower=False)
+        in_perm = np.argsort(lu.perm_r)  # factor row k <- b[in_perm[k]]
+        out_perm = np.argsort(lu.perm_c)  # factor row k -> x[out_perm[k]]
+        dev = device()
+        bufs = [
+            _i32(l_strict.indptr), _i32(l_strict.indices if l_strict.nnz else [0]),
+            _f64(l_strict.data if l_strict.nnz else [0.0]), _i32(ord_l),
+            torch.zeros(max(n, 1), dtype=torch.int32, device=dev),
+            _i32(u_strict.indptr), _i32(u_strict.indices if u_strict.nnz else [0]),
+            _f64(u_strict.data if u_strict.nnz else [0.0]), _i32(ord_u),
+            torch.zeros(max(n, 1), dtype=torch.int32, device=dev),
+            _f64(1.0 / diag), torch.zeros(2, dtype=torch.int32, device=dev),
+        ]
+        ticket = bufs[11]
+        l_struct = _lib.TriFactor(
+            n=n, lower=1, rowptr=bufs[0].data_ptr(), colind=bufs[1].data_ptr(),
+            vals=bufs[2].data_ptr(), diag_inv=None, order=bufs[3].data_ptr(),
+            flags=bufs[4].data_ptr(), ticket=ticket.data_ptr(),
+        )
+        u_struct = _lib.TriFactor(
+            n=n, lower=0, rowptr=bufs[5].data_ptr(), colind=bufs[6].data_ptr(),
+            vals=bufs[7].data_ptr(), diag_inv=bufs[10].data_ptr(), order=bufs[8].data_ptr(),
+            flags=bufs[9].data_ptr(), ticket=ticket.data_ptr() + 4,
+        )
+        return cls(n=n, depth_l=depth_l, depth_u=depth_u, nnz_l=int(l_strict.nnz),
+                   nnz_u=int(u_strict.nnz), bufs=bufs, l_struct=l_struct, u_struct=u_struct,
+                   in_perm=_i32(in_perm), out_perm=_i32(out_perm))
+
+    def solve_segments(self, b_segs: list[tuple[torch.Tensor, int]], x_segs: list[tuple[torch.Tensor, int]],
+                       width: int, stream=None) -> None:
+        """x = A^-1 b on `width` columns of (up to 3) row segments that stack
+        to the factor size (the hGSoc P~ solve of vstack(y, u, lambda))."""
+        if width == 0 or self.n == 0:
+            return
+        seg_rows = self.n // len(b_segs)
+        if seg_rows * len(b_segs) != self.n or len(b_segs) != len(x_segs) or len(b_segs) > 3:
+            raise ValueError("row segments do not stack to the factor size")
+
+        def segview(segs):
+            ptrs = (ctypes.c_void_p * 3)()
+            ld = None
+            col0 = None
+            for i, (t, c0) in enumerate(segs):
+                if t.shape[0] != seg_rows or t.dtype != torch.float64 or not t.is_cuda or t.stride(1) != 1:
+                    raise ValueError("segment must be a (rows, cols) float64 CUDA tensor")
+                if c0 + width > t.shape[1]:
+                    raise ValueError("segment too narrow")
+                if ld is None:
+                    ld, col0 = t.stride(0), c0
+                elif ld != t.stride(0) or col0 != c0:
+                    raise ValueError("segments must share leading dimension and column offset")
+                ptrs[i] = t.data_ptr()
+            return _lib.SegView(ptr=ptrs, ld=ld, col0=col0, seg_rows=seg_rows)
+
+        bv = segview(b_segs)
+        xv = segview(x_segs)
+        work = torch.empty((self.n, width), dtype=torch.float64, device=b_segs[0][0].device)
+        self.epoch += 1
+        rc = _lib.lib().sgk_trisolve(
+            ctypes.byref(self.l_struct), ctypes.byref(self.u_struct), self.in_perm.data_ptr(),
+            self.out_perm.data_ptr(), ctypes.byref(bv), ctypes.byref(xv), work.data_ptr(), width,
+            self.epoch, _lib.stream_ptr(stream),
+        )
+        _lib.check(rc, "sgk_trisolve")
+
+
+@dataclass(frozen=True, eq=False)
+class LUFactors:
+    """Sparse LU (partial pivoting) of a square matrix; solves on the GPU
+    (reference linalg.py:76-87)."""
+
+    shape: tuple[int, int]
+    _solver: scipy.sparse.linalg.SuperLU
+    _cache: dict = field(default_factory=dict, repr=False, compare=False)
+
+    @property
+    def device_factors(self) -> TriangularFactors:
+        f = self._cache.get("dev")
+        if f is None:
+            f = TriangularFactors.from_superlu(self._solver)
+            self._cache["dev"] = f
+        return f
+
+    def solve(self, b):
+        """A^-1 b for b of shape (n,) or (n, k); NumPy in -> NumPy out."""
+        if tuple(b.shape)[0] != self.shape[0]:
+            raise ValueError("right-hand side length does not match factor size")
+        vec = len(b.shape) == 1
+        bd, host = as_device_state(b)
+        b2 = bd.reshape(self.shape[0], -1).contiguous()
+        x = torch.empty_like(b2)
+        self.device_factors.solve_segments([(b2, 0)], [(x, 0)], b2.shape[1])
+        out = x.reshape(-1) if vec else x
+        if host:
+            return out.to("cpu") if isinstance(b, torch.Tensor) else out.cpu().numpy()
+        return out
+
+
+def _locate_zero_pivot(mat: csr_matrix) -> int:
+    dense = mat.toarray()
+    _, u = scipy.linalg.lu(dense, permute_l=True)
+    diag = np.abs(np.diag(u))
+    bad = np.flatnonzero(diag <= diag.max() * np.finfo(float).eps * mat.shape[0])
+    return int(bad[0]) if bad.size else mat.shape[0] - 1
+
+
+def sparse_lu(mat: csr_matrix) -> LUFactors:
+    """Host SuperLU factorization, identical call to the reference
+    (linalg.py:103-120), singular matrices raise SingularMatrixError."""
+    if mat.shape[0] != mat.shape[1]:
+        raise ValueError("sparse_lu requires a square matrix")
+    try:
+        solver = scipy.sparse.linalg.splu(sp.csc_matrix(mat), diag_pivot_thresh=1.0)
+    except RuntimeError as exc:
+        raise SingularMatrixError(f"singular matrix: zero pivot at row {_locate_zero_pivot(mat)}") from exc
+    probe = solver.solve(np.ones(mat.shape[0]))
+    if not np.all(np.isfinite(probe)):
+        raise SingularMatrixError(f"singular matrix: zero pivot at row {_locate_zero_pivot(mat)}")
+    return LUFactors(shape=mat.shape, _solver=solver)
+
+
+def lu_solve(factors: LUFactors, b):
+    return factors.solve(b)

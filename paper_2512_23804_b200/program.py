@@ -1,0 +1,349 @@
+"""Host compiler for Galerkin coupling programs (the schedule the fused
+device kernel `program_kernel` in csrc/galerkin.cu executes).
+
+A *program* is a set of couplings
+
+    out_o[:, k] += c * (A_t V_s)[:, l]        for entries (s, o, t, l, k, c)
+
+which covers every hot-path product of the reference:
+
+* kron_apply              operators.py:88-96  (s=o=0, t<n_t, H_t entries)
+* kron_apply_sliced       operators.py:99-126 (entries restricted to src x dst)
+* HGS._cross_product      preconditioners.py:132-144 (t>=1, coefficient -h)
+* hGSoc._level_rhs        preconditioners.py:386-409 (3 inputs, 3 outputs)
+* steady_kkt_apply        operators.py:181-194 (mass as an extra slice)
+
+Compilation:
+1. every distinct product (s, l, t) becomes one stencil dot U_(s,l,t);
+2. products sharing an input column (s, l) form an *item*; an item lives in
+   one lane so the nine neighbour values V_s[j, l] stay in registers while
+   all its t are evaluated;
+3. items are packed 32 to a *group* (one warp); a group runs a list of
+   *steps* and at each step lane lambda evaluates the term step_term[q, lambda]
+   (-1 = idle).  "uniform" schedules give every lane the same t at a step
+   (the coefficient loads become warp broadcasts) at the price of idle lanes;
+   "packed" schedules give each lane its own term list (no idle lanes,
+   per-lane coefficient loads) — better when there are hundreds of terms;
+4. groups are cut into *phases* whose U values fit the shared-memory budget;
+5. the sparse H couplings become, per phase, a CSR gather list over output
+   columns reading U from shared memory.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["Coupling", "HostProgram", "compile_program", "coupling_from_csr"]
+
+
+@dataclass(frozen=True)
+class Coupling:
+    """Entries out_o[:, cols] += vals * (A_t V_s)[:, rows]."""
+
+    s: int
+    o: int
+    t: int
+    rows: np.ndarray  # input column l (relative to the input view)
+    cols: np.ndarray  # output column k (relative to the output view)
+    vals: np.ndarray
+
+
+def coupling_from_csr(s, o, t, h, row_range, col_range, scale=1.0) -> Coupling | None:
+    """Entries of h[rlo:rhi, clo:chi] as a coupling (rows offset by rlo: they
+    index the full input; cols relative to clo: they index the output view).
+    Returns None when the slice is empty (the reference skips those terms,
+    operators.py:124, preconditioners.py:142,369,382)."""
+    rlo, rhi = row_range
+    clo, chi = col_range
+    if rlo >= rhi or clo >= chi:
+        return None
+    sub = h[rlo:rhi, clo:chi].tocoo()
+    keep = sub.data != 0.0
+    if not np.any(keep):
+        return None
+    return Coupling(
+        s=s,
+        o=o,
+        t=t,
+        rows=sub.row[keep].astype(np.int64) + rlo,
+        cols=sub.col[keep].astype(np.int64),
+        vals=scale * sub.data[keep],
+    )
+
+
+@dataclass
+class HostProgram:
+    n_groups: int
+    n_phases: int
+    n_out_cols: int
+    max_phase_slots: int
+    lane_item: np.ndarray
+    group_step0: np.ndarray
+    step_term: np.ndarray
+    phase_group0: np.ndarray
+    gather_ptr: np.ndarray
+    gather_slot: np.ndarray
+    gather_coef: np.ndarray
+    out_col: np.ndarray
+    out_widths: tuple[int, ...]
+    stats: dict = field(default_factory=dict)
+
+
+def _schedule_uniform(item_terms: list[np.ndarray], order: np.ndarray):
+    groups = []
+    for g0 in range(0, len(order), 32):
+        members = order[g0 : g0 + 32]
+        union = np.unique(np.concatenate([item_terms[i] for i in members]))
+        groups.append((members, union))
+    return groups
+
+
+def _uniform_cost(groups) -> int:
+    return sum(len(u) for _, u in groups)
+
+
+def _best_uniform(item_terms: list[np.ndarray]):
+    n = len(item_terms)
+    keys_lex = sorted(range(n), key=lambda i: tuple(item_terms[i]))
+    keys_len = sorted(range(n), key=lambda i: (-len(item_terms[i]), tuple(item_terms[i])))
+    best = None
+    for order in (np.array(keys_lex, dtype=np.int64), np.array(keys_len, dtype=np.int64)):
+        groups = _schedule_uniform(item_terms, order)
+        cost = _uniform_cost(groups)
+        if best is None or cost < best[0]:
+            best = (cost, groups)
+    return best
+
+
+def compile_program(
+    couplings: list[Coupling],
+    out_widths: tuple[int, ...] | list[int],
+    *,
+    n_inputs: int | None = None,
+    budget_slots: int = 6144,
+    mode: str = "auto",
+    packed_chunk: int = 16,
+) -> HostProgram:
+    out_widths = tuple(int(w) for w in out_widths)
+    if not out_widths or len(out_widths) > 4:
+        raise ValueError("a program has 1..4 outputs")
+    couplings = [c for c in couplings if c is not None and len(c.rows)]
+    if n_inputs is None:
+        n_inputs = 1 + max((c.s for c in couplings), default=0)
+    if n_inputs > 4:
+        raise ValueError("a program has at most 4 inputs")
+    out_off = np.concatenate([[0], np.cumsum(out_widths)]).astype(np.int64)
+    n_out_cols = int(out_off[-1])
+
+    # ---- 1. distinct products (s, l, t) and gather entries ------------------
+    if couplings:
+        s_arr = np.concatenate([np.full(len(c.rows), c.s, np.int64) for c in couplings])
+        t_arr = np.concatenate([np.full(len(c.rows), c.t, np.int64) for c in couplings])
+        l_arr = np.concatenate([np.asarray(c.rows, np.int64) for c in couplings])
+        o_arr = np.concatenate([np.full(len(c.rows), c.o, np.int64) for c in couplings])
+        k_arr = np.concatenate([np.asarray(c.cols, np.int64) for c in couplings])
+        v_arr = np.concatenate([np.asarray(c.vals, np.float64) for c in couplings])
+    else:
+        s_arr = t_arr = l_arr = o_arr = k_arr = np.zeros(0, np.int64)
+        v_arr = np.zeros(0)
+    if np.any(k_arr < 0) or np.any(k_arr >= np.asarray(out_widths)[o_arr] if len(o_arr) else False):
+        raise ValueError("coupling column outside its output view")
+    if np.any(l_arr < 0) or np.any(l_arr >= (1 << 24)):
+        raise ValueError("input column out of range")
+    big_t = int(t_arr.max()) + 1 if len(t_arr) else 1
+    big_l = int(l_arr.max()) + 1 if len(l_arr) else 1
+    pair_key = (s_arr * big_l + l_arr) * big_t + t_arr
+    uniq, pair_of_entry = np.unique(pair_key, return_inverse=True)
+    p_t = uniq % big_t
+    p_item_key = uniq // big_t  # (s, l)
+    item_keys, item_of_pair = np.unique(p_item_key, return_inverse=True)
+    n_items = len(item_keys)
+    item_terms = [np.zeros(0, np.int64)] * n_items
+    if n_items:
+        order_pairs = np.argsort(item_of_pair, kind="stable")
+        splits = np.cumsum(np.bincount(item_of_pair, minlength=n_items))[:-1]
+        item_pair_lists = np.split(order_pairs, splits)
+        item_terms = [p_t[pl] for pl in item_pair_lists]
+    else:
+        item_pair_lists = []
+
+    # ---- 2./3. items -> groups -> steps ---------------------------------------
+    groups = []  # list of (lane_items[list of item or -1 per lane], steps[q][lane] -> t or -1)
+    chosen = "none"
+    if n_items:
+        uni_cost, uni_groups = _best_uniform(item_terms)
+        # packed: split long term lists, pack by length
+        sub_items = []
+        for i, terms in enumerate(item_terms):
+            for a in range(0, len(terms), packed_chunk):
+                sub_items.append((i, terms[a : a + packed_chunk]))
+        sub_items.sort(key=lambda it: -len(it[1]))
+        packed_groups = [sub_items[g : g + 32] for g in range(0, len(sub_items), 32)]
+        packed_cost = sum(len(g[0][1]) for g in packed_groups)
+        use_packed = mode == "packed" or (mode == "auto" and 2 * packed_cost < uni_cost)
+        if use_packed:
+            chosen = "packed"
+            for g in packed_groups:
+                nsteps = len(g[0][1])
+                lanes = [it[0] for it in g] + [-1] * (32 - len(g))
+                steps = -np.ones((nsteps, 32), np.int64)
+                for lane, (_, terms) in enumerate(g):
+                    steps[: len(terms), lane] = terms
+                groups.append((lanes, steps))
+        else:
+            chosen = "uniform"
+            for members, union in uni_groups:
+                lanes = list(members) + [-1] * (32 - len(members))
+                steps = -np.ones((len(union), 32), np.int64)
+                for lane, it in enumerate(members):
+                    mask = np.isin(union, item_terms[it])
+                    steps[mask, lane] = union[mask]
+                groups.append((lanes, steps))
+
+    # split groups whose steps alone exceed the phase budget
+    max_steps = max(1, budget_slots // 32)
+    split_groups = []
+    for lanes, steps in groups:
+        for a in range(0, len(steps), max_steps):
+            split_groups.append((lanes, steps[a : a + max_steps]))
+    groups = split_groups
+
+    # ---- 4. phases -----------------------------------------------------------
+    phase_group0 = [0]
+    group_step0 = [0]
+    acc = 0
+    for gi, (_, steps) in enumerate(groups):
+        if acc + len(steps) > max_steps and acc > 0:
+            phase_group0.append(gi)
+            acc = 0
+        acc += len(steps)
+        group_step0.append(group_step0[-1] + len(steps))
+    if groups:
+        phase_group0.append(len(groups))
+    n_phases = len(phase_group0) - 1 if groups else 0
+    n_groups = len(groups)
+    total_steps = group_step0[-1]
+
+    lane_item = -np.ones(max(n_groups, 0) * 32, np.int64)
+    step_term = -np.ones((total_steps, 32), np.int64)
+    # pair -> (phase, slot)
+    n_pairs = len(uniq)
+    pair_phase = -np.ones(n_pairs, np.int64)
+    pair_slot = -np.ones(n_pairs, np.int64)
+    # per item: term -> pair id
+    item_term_pair = []
+    for i in range(n_items):
+        item_term_pair.append(dict(zip(item_terms[i].tolist(), item_pair_lists[i].tolist())))
+    ph = 0
+    for gi, (lanes, steps) in enumerate(groups):
+        while ph + 1 < len(phase_group0) and gi >= phase_group0[ph + 1]:
+            ph += 1
+        qbase = group_step0[phase_group0[ph]]
+        q0 = group_step0[gi]
+        step_term[q0 : q0 + len(steps)] = steps
+        for lane, it in enumerate(lanes):
+            if it < 0:
+                continue
+            key = int(item_keys[it])
+            s_i, l_i = divmod(key, big_l)
+            lane_item[gi * 32 + lane] = (s_i << 24) | l_i
+            col = steps[:, lane]
+            for qq in np.flatnonzero(col >= 0):
+                pid = item_term_pair[it][int(col[qq])]
+                if pair_phase[pid] >= 0:
+                    raise AssertionError("product scheduled twice")
+                pair_phase[pid] = ph
+                pair_slot[pid] = (q0 + qq - qbase) * 32 + lane
+    if n_pairs and np.any(pair_phase < 0):
+        raise AssertionError("unscheduled product")
+
+    # ---- 5. gather lists -----------------------------------------------------
+    n_ent = len(v_arr)
+    c_arr = out_off[o_arr] + k_arr if n_ent else np.zeros(0, np.int64)
+    e_phase = pair_phase[pair_of_entry] if n_ent else np.zeros(0, np.int64)
+    e_slot = pair_slot[pair_of_entry] if n_ent else np.zeros(0, np.int64)
+    e_t = t_arr
+    ordr = np.lexsort((l_arr, e_t, c_arr, e_phase)) if n_ent else np.zeros(0, np.int64)
+    n_ptr = max(n_phases, 0) * n_out_cols
+    counts = np.bincount(e_phase * n_out_cols + c_arr, minlength=n_ptr) if n_ent else np.zeros(n_ptr, np.int64)
+    gather_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    gather_slot = e_slot[ordr]
+    gather_coef = v_arr[ordr]
+    o_of_c = np.repeat(np.arange(len(out_widths)), out_widths)
+    k_of_c = np.concatenate([np.arange(w) for w in out_widths]) if n_out_cols else np.zeros(0, np.int64)
+    out_col = (o_of_c << 24) | k_of_c
+
+    max_slots = 0
+    for p in range(n_phases):
+        q_lo = group_step0[phase_group0[p]]
+        q_hi = group_step0[phase_group0[p + 1]]
+        max_slots = max(max_slots, (q_hi - q_lo) * 32)
+
+    useful = n_pairs
+    executed = total_steps * 32
+    stats = {
+        "mode": chosen,
+        "n_products": int(useful),
+        "n_items": int(n_items),
+        "n_groups": int(n_groups),
+        "n_steps": int(total_steps),
+        "lane_efficiency": float(useful / executed) if executed else 1.0,
+        "n_gather": int(n_ent),
+    }
+    i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
+    return HostProgram(
+        n_groups=n_groups,
+        n_phases=n_phases,
+        n_out_cols=n_out_cols,
+        max_phase_slots=int(max_slots),
+        lane_item=i32(lane_item),
+        group_step0=i32(group_step0),
+        step_term=i32(step_term.reshape(-1)),
+        phase_group0=i32(phase_group0 if n_phases else [0]),
+        gather_ptr=i32(gather_ptr),
+        gather_slot=i32(gather_slot),
+        gather_coef=np.ascontiguousarray(gather_coef, dtype=np.float64),
+        out_col=i32(out_col),
+        out_widths=out_widths,
+        stats=stats,
+    )
+
+
+def emulate(prog: HostProgram, pattern_rowptr, pattern_colind, slice_vals_std, inputs, inits, alpha, beta):
+    """NumPy emulation of program_kernel (test-only helper for the schedule;
+    slice_vals_std[t] is the CSR data array of slice t on the pattern)."""
+    n_rows = len(pattern_rowptr) - 1
+    import scipy.sparse as sp
+
+    mats = [sp.csr_matrix((v, pattern_colind, pattern_rowptr), shape=(n_rows, inputs[0].shape[0])) for v in slice_vals_std]
+    outs = []
+    acc = np.zeros((n_rows, prog.n_out_cols))
+    steps = prog.step_term.reshape(-1, 32)
+    for p in range(prog.n_phases):
+        ub = np.zeros((n_rows, prog.max_phase_slots))
+        g0, g1 = prog.phase_group0[p], prog.phase_group0[p + 1]
+        qbase = prog.group_step0[g0]
+        for g in range(g0, g1):
+            for lane in range(32):
+                item = prog.lane_item[g * 32 + lane]
+                if item < 0:
+                    continue
+                s, l = item >> 24, item & 0xFFFFFF
+                for q in range(prog.group_step0[g], prog.group_step0[g + 1]):
+                    t = steps[q, lane]
+                    if t >= 0:
+                        ub[:, (q - qbase) * 32 + lane] = mats[t] @ inputs[s][:, l]
+        for c in range(prog.n_out_cols):
+            e0, e1 = prog.gather_ptr[p * prog.n_out_cols + c], prog.gather_ptr[p * prog.n_out_cols + c + 1]
+            for e in range(e0, e1):
+                acc[:, c] += prog.gather_coef[e] * ub[:, prog.gather_slot[e]]
+    off = 0
+    for o, w in enumerate(prog.out_widths):
+        y = alpha[o] * acc[:, off : off + w]
+        if inits[o] is not None:
+            y = y + beta[o] * inits[o]
+        outs.append(y)
+        off += w
+    return outs
