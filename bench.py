@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path (BASELINE.json metric: "Galerkin matvec GB/s
+vs HBM peak; hGSoc-MINRES time-to-solution + iterations").
+
+Headline line (one JSON object on rank 0):
+  * workload = BASELINE config 4 (the matvec stress test: N=65025, n_xi=1001,
+    n_t=11, V ~ N(0,1) seeded, 520 MB > L2 so every timed matvec streams HBM);
+  * a "step" = one Galerkin matvec W = sum_t A_t V H_t over the whole V;
+  * value = algorithmic GB/s = B / t, B = 16 N n_xi + 8 n_t nnz(A)
+    + 4 (nnz(A)+N+1) + 12 sum nnz(H_t)  (1095.3 MB at cfg4),
+    whole job over all ranks (weak scaling: each rank its own matvecs);
+  * e2e = same metric through the public drop-in API `kron_apply` with V in
+    pinned host memory: H2D(V) + kernel + D2H(W) inside the timed region;
+  * roofline = the fused program_kernel vs the measured HBM copy peak;
+  * cpu_baseline = the NumPy/SciPy oracle port of the reference path on a
+    bounded row sample of the same workload, on this host;
+  * solves = time-to-solution + iterations for config 2 (hGSoc-FGMRES and
+    block-diagonal-hGS MINRES, tol 1e-8) — and config 5 with --solve-cfg5.
+
+`--impl reference` times the oracle port (the reference is pure Python /
+SciPy; there is no compiled reference) on the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SEED = 20240817
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded or sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows),
+                "power_w_max": max((float(r[3]) for r in rows if _isnum(r[3])), default=None)}
+
+
+def _isnum(s):
+    try:
+        float(s)
+        return True
+    except ValueError:
+        return False
+
+
+def matvec_bytes(n_h, n_xi, n_t, nnz_a, nnz_h):
+    return 16 * n_h * n_xi + 8 * n_t * nnz_a + 4 * (nnz_a + n_h + 1) + 12 * nnz_h
+
+
+def cpu_sample(bundle, x, budget_s=3.0):
+    """Oracle port (reference algorithm) on a contiguous row slab; returns
+    (GB/s, seconds, rows, bytes)."""
+    import oracle
+
+    cp = bundle.triple.matrices[: bundle.n_terms]
+    n_h, n_xi = x.shape
+    rows = max(256, n_h // 64)
+    t0 = time.perf_counter()
+    oracle.kron_apply_rows(cp, bundle.stiffness, x, (0, rows))
+    dt = time.perf_counter() - t0
+    rows = int(min(n_h, max(rows, rows * budget_s / max(dt, 1e-3))))
+    r0 = (n_h - rows) // 2
+    a = bundle.stiffness[0][r0:r0 + rows]
+    touched = np.unique(a.indices).size
+    nnz = a.nnz
+    nnz_h = sum(int(h.nnz) for h in cp)
+    b = 8 * n_xi * (touched + rows) + 8 * bundle.n_terms * nnz + 4 * (nnz + rows + 1) + 12 * nnz_h
+    t0 = time.perf_counter()
+    oracle.kron_apply_rows(cp, bundle.stiffness, x, (r0, r0 + rows))
+    dt = time.perf_counter() - t0
+    return b / dt / 1e9, dt, rows, b
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if ws > 1 and rank != 0:
+        return
+    from paper_2512_23804_b200.problems import build_problem
+
+    bundle = build_problem(4)
+    x = np.random.default_rng(SEED).standard_normal((bundle.n_h, bundle.n_xi))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        gbs, dt, rows, b = cpu_sample(bundle, x, budget_s=args.ref_budget)
+        if i >= args.warmup:
+            vals.append((gbs, dt, rows, b))
+    value = statistics.median(v[0] for v in vals)
+    rows = vals[-1][2]
+    line = {
+        "impl": "reference",
+        "metric": "galerkin_matvec_gbs",
+        "value": value,
+        "unit": "GB/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.median(v[1] for v in vals),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded N(0,1) V, BASELINE cfg4 operators)",
+        "config": {"workload": "cfg4 Galerkin matvec, row sample", "n_h": bundle.n_h, "n_xi": bundle.n_xi,
+                   "n_t": bundle.n_terms, "sample_rows": rows},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "port",
+                         "sample": f"rows [{(bundle.n_h - rows) // 2}, +{rows}) of the cfg4 matvec per step; "
+                                   "NumPy/SciPy restatement of sgkkt kron_apply (scipy sparsetools holds the GIL: 1 core)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _event_time(fn, steps, stream):
+    import torch
+
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(steps):
+        fn()
+    end.record(stream)
+    end.synchronize()
+    return start.elapsed_time(end) / 1e3
+
+
+def solve_block(cfg_id, betas, with_cpu=False):
+    """Time-to-solution of the control configs on the GPU (setup reported
+    separately)."""
+    import torch
+
+    from paper_2512_23804_b200.krylov import FgmresConfig, fgmres, minres
+    from paper_2512_23804_b200.operators import steady_kkt_apply_device
+    from paper_2512_23804_b200.preconditioners import build_coupled_preconditioner, build_steady_preconditioner
+    from paper_2512_23804_b200.problems import build_problem, steady_system
+
+    out = {}
+    t0 = time.perf_counter()
+    bundle = build_problem(cfg_id)
+    t_asm = time.perf_counter() - t0
+    for beta in betas:
+        sys_ = steady_system(bundle, beta=beta)
+        n = sys_.block_size()
+        shape = (sys_.n_h, sys_.n_xi)
+        rhs = np.zeros(3 * n)
+        rhs[:n] = np.asarray(sys_.mass @ sys_.target).ravel()
+        b = torch.as_tensor(rhs).cuda()
+
+        def split(v):
+            return [v[i * n:(i + 1) * n].view(shape) for i in range(3)]
+
+        def op(v):
+            o = torch.empty_like(v)
+            steady_kkt_apply_device(sys_, *split(v), tuple(split(o)))
+            return o
+
+        rec = {}
+        for name, builder, solver in (
+            ("hgsoc_fgmres", lambda: build_coupled_preconditioner(sys_, bundle.partition), fgmres),
+            ("blockdiag_hgs_minres", lambda: build_steady_preconditioner(sys_, bundle.partition, "cheb5"), minres),
+        ):
+            t0 = time.perf_counter()
+            prec = builder()
+            # first apply compiles programs and uploads factors (setup)
+            warm = torch.zeros(3 * n, dtype=torch.float64, device="cuda")
+            warm[0] = 1.0
+            prec.apply_device(*split(warm), outs=tuple(split(torch.empty_like(warm))))
+            torch.cuda.synchronize()
+            t_setup = time.perf_counter() - t0
+
+            def pr(v, prec=prec):
+                o = torch.empty_like(v)
+                prec.apply_device(*split(v), outs=tuple(split(o)))
+                return o
+
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            x, rep = solver(op, pr, b, FgmresConfig(tol=1e-8, max_iters=500))
+            torch.cuda.synchronize()
+            t_solve = time.perf_counter() - t0
+            r = op(x)
+            true_res = float(torch.linalg.vector_norm(b - r) / torch.linalg.vector_norm(b))
+            rec[name] = {"iterations": rep.iterations, "converged": bool(rep.converged),
+                         "seconds": t_solve, "setup_seconds": t_setup, "true_rel_residual": true_res}
+        out[f"beta={beta:g}"] = rec
+    out["assembly_seconds"] = t_asm
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_23804_b200 import _lib
+    from paper_2512_23804_b200.operators import kron_apply
+    from paper_2512_23804_b200.preconditioners import build_sweep
+    from paper_2512_23804_b200.problems import build_problem
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    bundle = build_problem(4)
+    cp = bundle.triple.matrices[: bundle.n_terms]
+    from paper_2512_23804_b200.operators import KroneckerSumOperator
+
+    op = KroneckerSumOperator(couplings=cp, operators=bundle.stiffness)
+    rng = np.random.default_rng(SEED + rank)
+    x_host = rng.standard_normal((bundle.n_h, bundle.n_xi))
+    x = torch.as_tensor(x_host).to(dev)
+    w = torch.empty_like(x)
+    nnz_h = sum(int(h.nnz) for h in cp)
+    B = matvec_bytes(bundle.n_h, bundle.n_xi, bundle.n_terms, bundle.stiffness[0].nnz, nnz_h)
+    assert B == op.algorithmic_bytes()
+    from paper_2512_23804_b200.device import run_program
+
+    prog = op.program([(0, bundle.n_xi)], (0, bundle.n_xi), 0, op.n_terms)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        run_program(op.pattern, prog, [(x, 0)], [(w, 0)], alpha=[1.0], beta=[0.0])
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    # correctness spot-check on a row slab against the oracle (outside the timed region)
+    import oracle
+
+    r0 = bundle.n_h // 2
+    ref = oracle.kron_apply_rows(cp, bundle.stiffness, x_host, (r0, r0 + 64))
+    got = w[r0:r0 + 64].cpu().numpy()
+    spot_err = float(np.abs(got - ref).max() / np.abs(ref).max())
+
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        t = _event_time(step, args.steps, stream)
+    launches = _lib.launch_count() - l0
+    torch.cuda.synchronize()
+    if ws > 1:
+        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+        dist.barrier()
+    value = ws * args.steps * B / t / 1e9
+    kernel_avg = t / args.steps
+
+    # e2e through the public API with pinned host buffers
+    xp = torch.from_numpy(x_host).pin_memory()
+    wp = torch.empty_like(xp).pin_memory()
+    for _ in range(2):
+        kron_apply(op, xp, out=wp)
+    torch.cuda.synchronize()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(e2e_steps):
+        kron_apply(op, xp, out=wp)
+    ev1.record(stream)
+    ev1.synchronize()
+    t_e2e = ev0.elapsed_time(ev1) / 1e3
+    e2e_err = float(np.abs(wp.numpy() - w.cpu().numpy()).max())
+    if ws > 1:
+        tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e_value = ws * e2e_steps * B / t_e2e / 1e9
+
+    peak, peak_kind = _peaks()
+    achieved = B / kernel_avg / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("program_kernel_cfg4_bytes")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "galerkin_matvec_gbs",
+        "value": value,
+        "unit": "GB/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * kernel_avg,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded N(0,1) V; BASELINE cfg4 operators: Q1 256x256 unit square, affine KL, Legendre m=10 p=4)",
+        "config": {"workload": "cfg4 Galerkin matvec W = sum_t A_t V H_t", "n_h": bundle.n_h, "n_xi": bundle.n_xi,
+                   "n_t": bundle.n_terms, "nnz_A": int(bundle.stiffness[0].nnz), "nnz_H": nnz_h,
+                   "algorithmic_bytes": B, "l2": "inputs larger than L2 (V 520.7 MB, W 520.7 MB per step)",
+                   "parallelism": f"replica x{ws} (independent matvecs per GPU)",
+                   "spot_check_rel_err_vs_oracle": spot_err},
+        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": int(x.numel() * 8),
+                "d2h_bytes_per_step": int(w.numel() * 8), "api": "kron_apply(op, pinned CPU tensor, out=pinned)",
+                "max_abs_diff_vs_device": e2e_err},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_kind": peak_kind, "kernel": "program_kernel (cfg4 full matvec)",
+                     "fp64_flops_per_launch": None},
+        "clocks": clk.summary(),
+    }
+    prog_stats = prog.host.stats
+    line["config"]["schedule"] = prog_stats
+    # fp64 work actually issued per launch (the kernel is DFMA-heavy: SURVEY §7 H1)
+    useful = 2 * bundle.stiffness[0].nnz * prog_stats["n_products"] + 2 * bundle.n_h * prog_stats["n_gather"]
+    line["roofline"]["fp64_flops_per_launch"] = useful
+    line["roofline"]["fp64_tflops"] = useful / kernel_avg / 1e12
+    if rank == 0 and not args.no_cpu:
+        gbs, dt, rows, b = cpu_sample(bundle, x_host, budget_s=args.ref_budget)
+        line["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "port",
+                                "sample": f"{rows} contiguous output rows of the cfg4 matvec ({b / 1e6:.1f} MB algorithmic, "
+                                          f"{dt:.2f} s); NumPy/SciPy oracle port of sgkkt kron_apply, 1 core (GIL-bound)"}
+    if rank == 0 and not args.no_solve:
+        solves = {"cfg2": solve_block(2, [1e-2])}
+        if args.solve_cfg5:
+            solves["cfg5"] = solve_block(5, [1e-2, 1e-4, 1e-6])
+        line["solves"] = solves
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--solve-cfg5", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=3.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -24,6 +24,7 @@ __all__ = [
     "fgmres",
     "hgs_apply",
     "kron_apply",
+    "kron_apply_rows",
     "kron_apply_sliced",
     "minres",
     "richardson_hgs",
@@ -383,3 +384,14 @@ def timed(fn, *args, **kw):
     t0 = time.perf_counter()
     out = fn(*args, **kw)
     return out, time.perf_counter() - t0
+
+
+def kron_apply_rows(couplings, operators, x, rows):
+    """kron_apply restricted to a contiguous row slab [r0, r1) of the output
+    (same per-term algorithm, operators.py:94-95); used for bounded CPU
+    baseline samples."""
+    r0, r1 = rows
+    out = np.zeros((r1 - r0, x.shape[1]))
+    for h, a in zip(couplings, operators):
+        out += _xh(a[r0:r1] @ x, h)
+    return out
