@@ -50,6 +50,8 @@ extern "C" {
 typedef struct {
   int32_t n_rows;
   int32_t n_slices;
+  int32_t max_row_nnz;   /* longest row (selects the staged kernel)      */
+  int32_t pad;
   const int32_t* rowptr; /* [n_rows+1] */
   const int32_t* colind; /* [nnz] sorted per row */
   const double* vals;    /* [nnz*n_slices] */
@@ -90,6 +92,53 @@ int sgk_program_apply(const sgk_pattern* pat, const sgk_program* prog,
                       const sgk_view* init, /* ptr may be NULL per output  */
                       const double* alpha, const double* beta,
                       int32_t block_threads, void* stream);
+
+/* Fast path for patterns with at most 9 entries per row (the Q1 stencil):
+ * every row padded to exactly 9 columns (padding entries carry a valid
+ * column and zero values); coefficients per row as n_slices blocks of 10
+ * doubles (16-byte aligned pairs, the 10th is zero).                        */
+typedef struct {
+  int32_t n_rows;
+  int32_t n_slices;
+  const int32_t* colind9; /* [n_rows*9]                                     */
+  const double* coef10;   /* [n_rows*n_slices*10]                           */
+} sgk_pattern9;
+
+/* Contiguous-group uniform schedule: group g covers input columns
+ * [col0, col0+ncols) (ncols <= 128) of input s; lane L of the owning warp
+ * holds columns col0 + 32c + L (c < 4).  Step q evaluates term t_q for the
+ * column slots c whose slot base sb_c >= 0 (32 U slots each).
+ * group_info[g] = {s, col0, ncols, q0};  step_rec[q] = {t, sb0, sb1, sb2,
+ * sb3, 0, 0, 0} (inactive slots point at the 32 trash slots n_ubuf..);
+ * gather in SELL-32 form: gather_ptr[2j], gather_ptr[2j+1] = entry count and
+ * offset of chunk j (32 output positions), entries at off + e*32 + lane,
+ * packed (slot << 14) | coef_index (padding reads the zero slots
+ * n_ubuf+32..); out_col[position] = (output<<24)|column or -1.              */
+typedef struct {
+  int32_t n_groups;
+  int32_t n_steps;
+  int32_t n_ubuf;
+  int32_t n_out_cols;
+  int32_t n_coef;
+  int32_t n_gather;
+  const int32_t* group_info; /* [(n_groups+1)*4]                            */
+  const int32_t* step_rec;   /* [n_steps*8]                                 */
+  const double* coef_tab;    /* [n_coef]                                    */
+  const int32_t* gather_ptr; /* [2*ceil(n_out_cols/32)]                     */
+  const uint32_t* gather_ent;/* [n_gather]                                  */
+  const int32_t* out_col;    /* [32*ceil(n_out_cols/32)]                    */
+} sgk_program9;
+
+/* Same contract as sgk_program_apply for a padded 9-point pattern.  Returns
+ * SGK_ELIMIT when the program does not fit in shared memory (use the
+ * general kernel then).                                                     */
+int sgk_stencil9_apply(const sgk_pattern9* pat, const sgk_program9* prog,
+                       int32_t n_in, const sgk_view* in,
+                       int32_t n_out, const sgk_view* out,
+                       const sgk_view* init, const double* alpha,
+                       const double* beta, int32_t block_threads, void* stream);
+/* Shared-memory bytes the fast path needs for (pattern, program).          */
+int64_t sgk_stencil9_smem_bytes(const sgk_pattern9* pat, const sgk_program9* prog);
 
 /* Sparse triangular factor (CSR, off-diagonal entries only) with a
  * dependency-respecting row order (level order).  diag_inv==NULL means

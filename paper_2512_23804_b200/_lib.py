@@ -41,6 +41,8 @@ class Pattern(ctypes.Structure):
     _fields_ = [
         ("n_rows", c_i32),
         ("n_slices", c_i32),
+        ("max_row_nnz", c_i32),
+        ("pad", c_i32),
         ("rowptr", c_vp),
         ("colind", c_vp),
         ("vals", c_vp),
@@ -61,6 +63,18 @@ class Program(ctypes.Structure):
         ("gather_slot", c_vp),
         ("gather_coef", c_vp),
         ("out_col", c_vp),
+    ]
+
+
+class Pattern9(ctypes.Structure):
+    _fields_ = [("n_rows", c_i32), ("n_slices", c_i32), ("colind9", c_vp), ("coef10", c_vp)]
+
+
+class Program9(ctypes.Structure):
+    _fields_ = [
+        ("n_groups", c_i32), ("n_steps", c_i32), ("n_ubuf", c_i32), ("n_out_cols", c_i32),
+        ("n_coef", c_i32), ("n_gather", c_i32), ("group_info", c_vp), ("step_rec", c_vp),
+        ("coef_tab", c_vp), ("gather_ptr", c_vp), ("gather_ent", c_vp), ("out_col", c_vp),
     ]
 
 
@@ -91,6 +105,11 @@ _SIGNATURES = {
                                   ctypes.POINTER(View), c_i32, ctypes.POINTER(View),
                                   ctypes.POINTER(View), ctypes.POINTER(c_dbl),
                                   ctypes.POINTER(c_dbl), c_i32, c_vp]),
+    "sgk_stencil9_apply": (c_i32, [ctypes.POINTER(Pattern9), ctypes.POINTER(Program9), c_i32,
+                                   ctypes.POINTER(View), c_i32, ctypes.POINTER(View),
+                                   ctypes.POINTER(View), ctypes.POINTER(c_dbl),
+                                   ctypes.POINTER(c_dbl), c_i32, c_vp]),
+    "sgk_stencil9_smem_bytes": (c_i64, [ctypes.POINTER(Pattern9), ctypes.POINTER(Program9)]),
     "sgk_trisolve": (c_i32, [ctypes.POINTER(TriFactor), ctypes.POINTER(TriFactor), c_vp, c_vp,
                              ctypes.POINTER(SegView), ctypes.POINTER(SegView), c_vp, c_i32,
                              c_i32, c_vp]),

@@ -26,20 +26,18 @@
 
 namespace sgk {
 
-struct ViewSet {
-  sgk_view v[SGK_MAX_IO];
-};
-struct ScalarSet {
-  double s[SGK_MAX_IO];
-};
+constexpr int kChunk = 9;          // stencil entries held in registers per pass
+constexpr int kStageMax = 2048;    // doubles of row coefficients staged in shared memory
 
-constexpr int kChunk = 9;  // stencil entries held in registers per pass
-
-template <int MAXOUT>
+// STAGED: the row's t-stacked coefficients (n_slices*len doubles) are copied
+// to shared memory once per row and read back as warp broadcasts.
+template <int MAXOUT, bool STAGED>
 __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_program prog,
                                                       ViewSet in, ViewSet out, ViewSet init,
                                                       ScalarSet alpha, ScalarSet beta) {
-  extern __shared__ double ubuf[];
+  extern __shared__ double smem[];
+  double* coef_s = smem;                          // [kStageMax] when STAGED
+  double* ubuf = smem + (STAGED ? kStageMax : 0);  // U slots of one phase
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -50,6 +48,12 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
     const int len = __ldg(pat.rowptr + row + 1) - rs;
     const double* arow = pat.vals + (int64_t)rs * n_slices;
     const int32_t* crow = pat.colind + rs;
+    if (STAGED) {
+      const int nco = n_slices * len;
+      for (int i = threadIdx.x; i < nco; i += blockDim.x) coef_s[i] = __ldg(arow + i);
+      __syncthreads();
+    }
+    const double* abase = STAGED ? coef_s : arow;
 
     double acc[MAXOUT];
 #pragma unroll
@@ -66,7 +70,7 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
         const double* vb = nullptr;
         int64_t ldv = 0;
         if (item >= 0) {
-          const sgk_view& vv = in.v[item >> 24];
+          const sgk_view& vv = pick(in, item >> 24);
           vb = vv.ptr + vv.col0 + (item & 0xFFFFFF);
           ldv = vv.ld;
         }
@@ -77,16 +81,41 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
 #pragma unroll
           for (int jj = 0; jj < kChunk; ++jj)
             v[jj] = (vb != nullptr && jj < cl) ? __ldg(vb + (int64_t)__ldg(crow + c0 + jj) * ldv) : 0.0;
-          for (int q = q0; q < q1; ++q) {
+          int q = q0;
+          // two independent steps per iteration (ILP across stencil dots)
+          for (; q + 1 < q1; q += 2) {
+            const int ta = __ldg(prog.step_term + q * 32 + lane);
+            const int tb = __ldg(prog.step_term + (q + 1) * 32 + lane);
+            const double* aa = abase + max(ta, 0) * len + c0;
+            const double* ab = abase + max(tb, 0) * len + c0;
+            double ua0 = 0.0, ua1 = 0.0, ub0 = 0.0, ub1 = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < kChunk; jj += 2) {
+              if (jj < cl) {
+                ua0 = fma(aa[jj], v[jj], ua0);
+                ub0 = fma(ab[jj], v[jj], ub0);
+              }
+              if (jj + 1 < cl) {
+                ua1 = fma(aa[jj + 1], v[jj + 1], ua1);
+                ub1 = fma(ab[jj + 1], v[jj + 1], ub1);
+              }
+            }
+            const int sa = (q - qbase) * 32 + lane;
+            if (ta >= 0) ubuf[sa] = (c0 == 0) ? ua0 + ua1 : ubuf[sa] + (ua0 + ua1);
+            if (tb >= 0) ubuf[sa + 32] = (c0 == 0) ? ub0 + ub1 : ubuf[sa + 32] + (ub0 + ub1);
+          }
+          if (q < q1) {
             const int t = __ldg(prog.step_term + q * 32 + lane);
             if (t >= 0) {
-              const double* at = arow + t * len + c0;
-              double u = 0.0;
+              const double* at = abase + t * len + c0;
+              double u0 = 0.0, u1 = 0.0;
 #pragma unroll
-              for (int jj = 0; jj < kChunk; ++jj)
-                if (jj < cl) u = fma(__ldg(at + jj), v[jj], u);
+              for (int jj = 0; jj < kChunk; jj += 2) {
+                if (jj < cl) u0 = fma(at[jj], v[jj], u0);
+                if (jj + 1 < cl) u1 = fma(at[jj + 1], v[jj + 1], u1);
+              }
               const int slot = (q - qbase) * 32 + lane;
-              ubuf[slot] = (c0 == 0) ? u : ubuf[slot] + u;
+              ubuf[slot] = (c0 == 0) ? u0 + u1 : ubuf[slot] + (u0 + u1);
             }
           }
         }
@@ -113,29 +142,30 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
       if (c < prog.n_out_cols) {
         const int oc = __ldg(prog.out_col + c);
         const int o = oc >> 24, k = oc & 0xFFFFFF;
-        double y = alpha.s[o] * acc[r];
-        const sgk_view& iv = init.v[o];
-        if (iv.ptr != nullptr) y += beta.s[o] * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
-        const sgk_view& ov = out.v[o];
+        double y = pick_s(alpha, o) * acc[r];
+        const sgk_view& iv = pick(init, o);
+        if (iv.ptr != nullptr) y += pick_s(beta, o) * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
+        const sgk_view& ov = pick(out, o);
         ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
       }
     }
+    if (STAGED && prog.n_phases == 0) __syncthreads();  // coef_s reuse guard
   }
 }
 
-template <int MAXOUT>
-static int launch_program(const sgk_pattern& pat, const sgk_program& prog, const ViewSet& in,
-                          const ViewSet& out, const ViewSet& init, const ScalarSet& alpha,
-                          const ScalarSet& beta, int threads, cudaStream_t st) {
-  const size_t smem = (size_t)prog.max_phase_slots * sizeof(double);
+template <int MAXOUT, bool STAGED>
+static int launch_program_t(const sgk_pattern& pat, const sgk_program& prog, const ViewSet& in,
+                            const ViewSet& out, const ViewSet& init, const ScalarSet& alpha,
+                            const ScalarSet& beta, int threads, cudaStream_t st) {
+  const size_t smem = (size_t)(prog.max_phase_slots + (STAGED ? kStageMax : 0)) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(program_kernel<MAXOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(program_kernel<MAXOUT, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr_set = true;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, program_kernel<MAXOUT>, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, program_kernel<MAXOUT, STAGED>, threads, smem);
   if (occ < 1) {
     set_error("program_kernel: zero occupancy (shared memory " + std::to_string(smem) + " B)");
     return SGK_ELIMIT;
@@ -143,8 +173,17 @@ static int launch_program(const sgk_pattern& pat, const sgk_program& prog, const
   int64_t grid = (int64_t)sm_count() * occ;
   if (grid > pat.n_rows) grid = pat.n_rows;
   if (grid < 1) return SGK_OK;
-  program_kernel<MAXOUT><<<(int)grid, threads, smem, st>>>(pat, prog, in, out, init, alpha, beta);
+  program_kernel<MAXOUT, STAGED><<<(int)grid, threads, smem, st>>>(pat, prog, in, out, init, alpha, beta);
   return check_launch("program_kernel");
+}
+
+template <int MAXOUT>
+static int launch_program(const sgk_pattern& pat, const sgk_program& prog, const ViewSet& in,
+                          const ViewSet& out, const ViewSet& init, const ScalarSet& alpha,
+                          const ScalarSet& beta, int threads, cudaStream_t st, int max_row_nnz) {
+  if ((int64_t)pat.n_slices * max_row_nnz <= kStageMax)
+    return launch_program_t<MAXOUT, true>(pat, prog, in, out, init, alpha, beta, threads, st);
+  return launch_program_t<MAXOUT, false>(pat, prog, in, out, init, alpha, beta, threads, st);
 }
 
 }  // namespace sgk
@@ -173,12 +212,13 @@ extern "C" int sgk_program_apply(const sgk_pattern* pat, const sgk_program* prog
   }
   if (pat->n_rows == 0 || prog->n_out_cols == 0) return SGK_OK;
   const int per = (prog->n_out_cols + threads - 1) / threads;
+  const int max_nnz = pat->max_row_nnz;
   cudaStream_t st = (cudaStream_t)stream;
-  if (per <= 1) return launch_program<1>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
-  if (per <= 2) return launch_program<2>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
-  if (per <= 4) return launch_program<4>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
-  if (per <= 8) return launch_program<8>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
-  if (per <= 16) return launch_program<16>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  if (per <= 1) return launch_program<1>(*pat, *prog, vin, vout, vinit, a, b, threads, st, max_nnz);
+  if (per <= 2) return launch_program<2>(*pat, *prog, vin, vout, vinit, a, b, threads, st, max_nnz);
+  if (per <= 4) return launch_program<4>(*pat, *prog, vin, vout, vinit, a, b, threads, st, max_nnz);
+  if (per <= 8) return launch_program<8>(*pat, *prog, vin, vout, vinit, a, b, threads, st, max_nnz);
+  if (per <= 16) return launch_program<16>(*pat, *prog, vin, vout, vinit, a, b, threads, st, max_nnz);
   set_error("sgk_program_apply: too many output columns for one CTA (max 16*block_threads)");
   return SGK_ELIMIT;
 }

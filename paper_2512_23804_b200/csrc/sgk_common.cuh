@@ -36,6 +36,32 @@ __device__ __forceinline__ void st_release(int32_t* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+struct ViewSet {
+  sgk_view v[SGK_MAX_IO];
+};
+struct ScalarSet {
+  double s[SGK_MAX_IO];
+};
+
+__device__ __forceinline__ const sgk_view& pick(const ViewSet& vs, int s) {
+  // constant-index selection keeps the views in the parameter bank (a
+  // dynamic index would spill the whole struct to local memory)
+  switch (s) {
+    case 0: return vs.v[0];
+    case 1: return vs.v[1];
+    case 2: return vs.v[2];
+    default: return vs.v[3];
+  }
+}
+__device__ __forceinline__ double pick_s(const ScalarSet& ss, int s) {
+  switch (s) {
+    case 0: return ss.s[0];
+    case 1: return ss.s[1];
+    case 2: return ss.s[2];
+    default: return ss.s[3];
+  }
+}
+
 }  // namespace sgk
 
 #define SGK_REQUIRE(cond, msg)        \

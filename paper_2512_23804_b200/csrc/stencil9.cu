@@ -1,0 +1,264 @@
+// K1/K2/K4 fast path — the coupling program on a padded 9-point stencil.
+//
+// Same contract as program_kernel (galerkin.cu), specialised for the Q1
+// pattern every BASELINE configuration uses (<= 9 entries per row):
+//   * each warp owns a group of 128 CONSECUTIVE chaos columns (lane L holds
+//     columns col0+L, +32, +64, +96), so the V loads of the 9 neighbour rows
+//     are 256-byte coalesced and the values stay in registers (36 doubles)
+//     while every term t of the group's step list is evaluated;
+//   * a step evaluates one term t for all four column slots that have any
+//     active (t, l) product: the 9 coefficients of A_t's row are read as 5
+//     warp-broadcast LDS.128 from the row's staged block and each feeds 4
+//     DFMAs (coefficient delivery, not DFMA, limits a 1-column-per-lane
+//     layout on B200: ~0.5 broadcast LDS/clk/SM vs 2 warp-DFMA/clk/SM);
+//   * the sparse H_t gather reads packed (slot, coefficient-index) entries
+//     that live in shared memory for the whole kernel (loaded once per CTA),
+//     so per row only the U values move through shared memory.
+// Rows are processed grid-stride by persistent CTAs; the row's coefficient
+// block (n_slices x 10 doubles) is staged with 16-byte loads.
+#include "sgk_common.cuh"
+
+namespace sgk {
+
+constexpr int kCols = 4;  // column slots per lane
+
+// Shared-memory map.  ubuf holds n_ubuf U slots + 32 trash slots (inactive
+// (step, column-slot) pairs store there) + 32 zero slots (gather padding).
+struct Smem9 {
+  size_t coef, cols, ubuf, ctab, steps, groups, ccnt, coff, gent, total;
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline Smem9 smem9_layout(int n_slices, const sgk_program9& p) {
+  Smem9 s;
+  size_t off = 0;
+  s.coef = off;   off = align16(off + 2 * sizeof(double) * (size_t)n_slices * 10);  // double buffer
+  s.cols = off;   off = align16(off + 2 * 16 * sizeof(int32_t));
+  s.ubuf = off;   off = align16(off + sizeof(double) * ((size_t)p.n_ubuf + 64));
+  s.ctab = off;   off = align16(off + sizeof(double) * (size_t)p.n_coef);
+  s.steps = off;  off = align16(off + sizeof(int32_t) * (size_t)p.n_steps);
+  s.groups = off; off = align16(off + sizeof(int32_t) * 4 * (size_t)(p.n_groups + 1));
+  const size_t n_chunks = ((size_t)p.n_out_cols + 31) / 32;
+  s.ccnt = off;   off = align16(off + sizeof(int32_t) * n_chunks);
+  s.coff = off;   off = align16(off + sizeof(int32_t) * n_chunks);
+  s.gent = off;   off = align16(off + sizeof(uint32_t) * (size_t)p.n_gather);
+  s.total = off;
+  return s;
+}
+
+// single accumulation chain: 1 DMUL + 8 DFMA, no extra adds on the FP64 pipe
+__device__ __forceinline__ double dot9(const double (&a)[10], const double (&v)[9]) {
+  double u = a[0] * v[0];
+#pragma unroll
+  for (int j = 1; j < 9; ++j) u = fma(a[j], v[j], u);
+  return u;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Gather layout (SELL-32): output positions are permuted on the host so that
+// 32 consecutive positions (a chunk, one warp) have similar entry counts;
+// chunk j has ccnt[j] entries per lane stored at gent[coff[j] + e*32 + lane];
+// out_col[position] maps back to (output, column) (-1 = padding lane).
+template <int MAXOUT>
+__global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
+                                                          ViewSet out, ViewSet init, ScalarSet alpha,
+                                                          ScalarSet beta) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const Smem9 L = smem9_layout(pat.n_slices, prog);
+  double* coef_s = reinterpret_cast<double*>(sm + L.coef);
+  int32_t* cols_s = reinterpret_cast<int32_t*>(sm + L.cols);
+  double* ubuf = reinterpret_cast<double*>(sm + L.ubuf);
+  double* ctab = reinterpret_cast<double*>(sm + L.ctab);
+  int32_t* steps = reinterpret_cast<int32_t*>(sm + L.steps);
+  int32_t* groups = reinterpret_cast<int32_t*>(sm + L.groups);
+  int32_t* ccnt = reinterpret_cast<int32_t*>(sm + L.ccnt);
+  int32_t* coff = reinterpret_cast<int32_t*>(sm + L.coff);
+  uint32_t* gent = reinterpret_cast<uint32_t*>(sm + L.gent);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int n_chunks = (prog.n_out_cols + 31) >> 5;
+  const int ncoef = pat.n_slices * 10;
+
+  // program tables -> shared memory, once per CTA
+  for (int i = tid; i < prog.n_coef; i += blockDim.x) ctab[i] = prog.coef_tab[i];
+  for (int i = tid; i < prog.n_steps; i += blockDim.x) steps[i] = prog.step_rec[i];
+  for (int i = tid; i < 4 * (prog.n_groups + 1); i += blockDim.x) groups[i] = prog.group_info[i];
+  for (int i = tid; i < n_chunks; i += blockDim.x) {
+    ccnt[i] = prog.gather_ptr[2 * i];
+    coff[i] = prog.gather_ptr[2 * i + 1];
+  }
+  for (int i = tid; i < prog.n_gather; i += blockDim.x) gent[i] = prog.gather_ent[i];
+  for (int i = tid; i < 64; i += blockDim.x) ubuf[prog.n_ubuf + i] = 0.0;
+
+  int ocol[MAXOUT];
+#pragma unroll
+  for (int r = 0; r < MAXOUT; ++r) {
+    const int chunk = warp + r * nwarps;
+    ocol[r] = chunk < n_chunks ? __ldg(prog.out_col + chunk * 32 + lane) : -1;
+  }
+
+  auto stage = [&](int row, int buf) {
+    const double* src = pat.coef10 + (int64_t)row * ncoef;
+    double* dst = coef_s + buf * ncoef;
+    for (int i = tid; i < ncoef / 2; i += blockDim.x) cp_async16(dst + 2 * i, src + 2 * i);
+    if (tid < 9) cp_async4(cols_s + 16 * buf + tid, pat.colind9 + (int64_t)row * 9 + tid);
+  };
+
+  int row = blockIdx.x;
+  if (row < pat.n_rows) stage(row, 0);
+  cp_async_commit();
+  for (int it = 0; row < pat.n_rows; row += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int next = row + gridDim.x;
+    if (next < pat.n_rows) stage(next, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();  // (A) this row's block visible; previous gather done with ubuf
+
+    const double* crow = coef_s + buf * ncoef;
+    const int32_t* cr = cols_s + 16 * buf;
+    int ubase = 0;  // slot base of group g: 128 slots per step, groups in order
+    for (int g = 0; g < warp && g < prog.n_groups; ++g)
+      ubase += 128 * (groups[4 * (g + 1) + 3] - groups[4 * g + 3]);
+    for (int g = warp; g < prog.n_groups; g += nwarps) {
+      const int4 gi = *reinterpret_cast<const int4*>(groups + 4 * g);
+      const int q1 = groups[4 * (g + 1) + 3];
+      const sgk_view& vv = pick(in, gi.x);
+      double v[kCols][9];
+      if (gi.z == 128) {
+        const double* base = vv.ptr + vv.col0 + gi.y + lane;
+#pragma unroll
+        for (int jj = 0; jj < 9; ++jj) {
+          const double* vr = base + (int64_t)cr[jj] * vv.ld;
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + 32 * c);
+        }
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 9; ++jj) {
+          const double* vr = vv.ptr + (int64_t)cr[jj] * vv.ld + vv.col0 + gi.y;
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + min(32 * c + lane, gi.z - 1));
+        }
+      }
+      double2* ub = reinterpret_cast<double2*>(ubuf + ubase + 4 * lane);
+      for (int q = gi.w; q < q1; ++q, ub += 64) {
+        const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[q]);
+        double a[10];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const double2 p = a2[k];
+          a[2 * k] = p.x;
+          a[2 * k + 1] = p.y;
+        }
+        ub[0] = make_double2(dot9(a, v[0]), dot9(a, v[1]));
+        ub[1] = make_double2(dot9(a, v[2]), dot9(a, v[3]));
+      }
+      // skip the slots of the groups owned by the other warps
+      for (int g2 = g; g2 < g + nwarps && g2 < prog.n_groups; ++g2)
+        ubase += 128 * (groups[4 * (g2 + 1) + 3] - groups[4 * g2 + 3]);
+    }
+    __syncthreads();  // (B) all U of this row in ubuf
+
+#pragma unroll
+    for (int r = 0; r < MAXOUT; ++r) {
+      const int chunk = warp + r * nwarps;
+      if (chunk >= n_chunks) break;
+      const int cnt = ccnt[chunk];
+      const uint32_t* ge = gent + coff[chunk] + lane;
+      double acc = 0.0;
+      for (int e = 0; e < cnt; ++e) {
+        const uint32_t w = ge[32 * e];
+        acc = fma(ctab[w & 0x3FFF], ubuf[w >> 14], acc);
+      }
+      const int oc = ocol[r];
+      if (oc >= 0) {
+        const int o = oc >> 24, k = oc & 0xFFFFFF;
+        double y = pick_s(alpha, o) * acc;
+        const sgk_view& iv = pick(init, o);
+        if (iv.ptr != nullptr) y += pick_s(beta, o) * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
+        const sgk_view& ov = pick(out, o);
+        ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
+      }
+    }
+  }
+  cp_async_wait1();
+}
+
+template <int MAXOUT>
+static int launch9(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
+                   const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int threads, cudaStream_t st) {
+  const Smem9 L = smem9_layout(pat.n_slices, prog);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(stencil9_kernel<MAXOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_kernel<MAXOUT>, threads, L.total);
+  if (occ < 1) {
+    set_error("stencil9_kernel: program does not fit in shared memory (" + std::to_string(L.total) + " B)");
+    return SGK_ELIMIT;
+  }
+  int64_t grid = (int64_t)sm_count() * occ;
+  if (grid > pat.n_rows) grid = pat.n_rows;
+  if (grid < 1) return SGK_OK;
+  stencil9_kernel<MAXOUT><<<(int)grid, threads, L.total, st>>>(pat, prog, in, out, init, a, b);
+  return check_launch("stencil9_kernel");
+}
+
+}  // namespace sgk
+
+extern "C" int64_t sgk_stencil9_smem_bytes(const sgk_pattern9* pat, const sgk_program9* prog) {
+  if (!pat || !prog) return -1;
+  return (int64_t)sgk::smem9_layout(pat->n_slices, *prog).total;
+}
+
+extern "C" int sgk_stencil9_apply(const sgk_pattern9* pat, const sgk_program9* prog, int32_t n_in,
+                                  const sgk_view* in, int32_t n_out, const sgk_view* out, const sgk_view* init,
+                                  const double* alpha, const double* beta, int32_t block_threads,
+                                  void* stream) {
+  using namespace sgk;
+  SGK_REQUIRE(pat && prog && out && alpha && beta, "sgk_stencil9_apply: null argument");
+  SGK_REQUIRE(n_in >= 0 && n_in <= SGK_MAX_IO && n_out >= 1 && n_out <= SGK_MAX_IO,
+              "sgk_stencil9_apply: input/output count out of range");
+  SGK_REQUIRE(prog->n_groups == 0 || n_in >= 1, "sgk_stencil9_apply: program needs inputs");
+  SGK_REQUIRE(prog->n_coef <= (1 << 14) && prog->n_ubuf <= (1 << 18),
+              "sgk_stencil9_apply: gather entry fields overflow");
+  const int threads = block_threads > 0 ? block_threads : 256;
+  SGK_REQUIRE(threads % 32 == 0 && threads <= 256, "sgk_stencil9_apply: block_threads must be a multiple of 32, <=256");
+  ViewSet vin{}, vout{}, vinit{};
+  ScalarSet a{}, b{};
+  for (int i = 0; i < n_in; ++i) vin.v[i] = in[i];
+  for (int i = 0; i < n_out; ++i) {
+    SGK_REQUIRE(out[i].ptr != nullptr, "sgk_stencil9_apply: null output");
+    vout.v[i] = out[i];
+    if (init) vinit.v[i] = init[i];
+    a.s[i] = alpha[i];
+    b.s[i] = beta[i];
+  }
+  if (pat->n_rows == 0 || prog->n_out_cols == 0) return SGK_OK;
+  const int per = ((prog->n_out_cols + 31) / 32 + threads / 32 - 1) / (threads / 32);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (per <= 1) return launch9<1>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  if (per <= 2) return launch9<2>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  if (per <= 4) return launch9<4>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  if (per <= 8) return launch9<8>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  if (per <= 16) return launch9<16>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  set_error("sgk_stencil9_apply: too many output columns for one CTA");
+  return SGK_ELIMIT;
+}

@@ -13,7 +13,7 @@ import scipy.sparse as sp
 import torch
 
 from . import _lib
-from .program import HostProgram
+from .program import HostProgram, HostProgram9, compile_program, compile_program9
 
 __all__ = [
     "DevicePattern",
@@ -24,6 +24,10 @@ __all__ = [
 ]
 
 F64 = torch.float64
+# set SGKKT_FAST9=0 to force the general program kernel (A/B testing)
+import os as _os
+
+FAST9 = _os.environ.get("SGKKT_FAST9", "1") != "0"
 
 
 def device() -> torch.device:
@@ -114,10 +118,34 @@ class DevicePattern:
         self.struct = _lib.Pattern(
             n_rows=n,
             n_slices=self.n_slices,
+            max_row_nnz=self.max_row_nnz,
+            pad=0,
             rowptr=self._rowptr.data_ptr(),
             colind=self._colind.data_ptr(),
             vals=self._vals.data_ptr(),
         )
+
+    def pattern9(self):
+        """Padded 9-entry layout for the fast path (None if a row is longer)."""
+        if self.max_row_nnz > 9:
+            return None
+        if getattr(self, "_p9", None) is None:
+            n, T = self.n_rows, self.n_slices
+            lens = np.diff(self.indptr)
+            row_of = np.repeat(np.arange(n), lens)
+            jj = np.arange(self.nnz) - self.indptr[row_of]
+            cols9 = np.zeros((n, 9), dtype=np.int64)
+            last = np.where(lens > 0, self.indices[np.maximum(self.indptr[1:] - 1, 0)], 0) if self.nnz else np.zeros(n, np.int64)
+            cols9[:] = last[:, None]
+            cols9[row_of, jj] = self.indices
+            coef = np.zeros((n, T, 10))
+            for t in range(T):
+                coef[row_of, t, jj] = self.slice_data[t]
+            self._colind9 = _i32(cols9)
+            self._coef10 = _f64(coef)
+            self._p9 = _lib.Pattern9(n_rows=n, n_slices=T, colind9=self._colind9.data_ptr(),
+                                     coef10=self._coef10.data_ptr())
+        return self._p9
 
     @property
     def algorithmic_bytes(self) -> int:
@@ -125,7 +153,7 @@ class DevicePattern:
         return 8 * self.n_slices * self.nnz + 4 * (self.nnz + self.n_rows + 1)
 
 
-class DeviceProgram:
+class _GenericProgram:
     def __init__(self, host: HostProgram):
         self.host = host
         self._bufs = [
@@ -140,23 +168,65 @@ class DeviceProgram:
         ]
         b = self._bufs
         self.struct = _lib.Program(
-            n_groups=host.n_groups,
-            n_phases=host.n_phases,
-            n_out_cols=host.n_out_cols,
-            max_phase_slots=host.max_phase_slots,
-            lane_item=b[0].data_ptr(),
-            group_step0=b[1].data_ptr(),
-            step_term=b[2].data_ptr(),
-            phase_group0=b[3].data_ptr(),
-            gather_ptr=b[4].data_ptr(),
-            gather_slot=b[5].data_ptr(),
-            gather_coef=b[6].data_ptr(),
-            out_col=b[7].data_ptr(),
+            n_groups=host.n_groups, n_phases=host.n_phases, n_out_cols=host.n_out_cols,
+            max_phase_slots=host.max_phase_slots, lane_item=b[0].data_ptr(), group_step0=b[1].data_ptr(),
+            step_term=b[2].data_ptr(), phase_group0=b[3].data_ptr(), gather_ptr=b[4].data_ptr(),
+            gather_slot=b[5].data_ptr(), gather_coef=b[6].data_ptr(), out_col=b[7].data_ptr(),
         )
+
+
+class _Program9:
+    def __init__(self, host: HostProgram9):
+        self.host = host
+        self._bufs = [
+            _i32(host.group_info), _i32(host.step_rec), _f64(host.coef_tab), _i32(host.gather_ptr),
+            torch.as_tensor(host.gather_ent.view(np.int32)).to(device()), _i32(host.out_col),
+        ]
+        b = self._bufs
+        self.struct = _lib.Program9(
+            n_groups=host.n_groups, n_steps=host.n_steps, n_ubuf=host.n_ubuf, n_out_cols=host.n_out_cols,
+            n_coef=host.n_coef, n_gather=host.n_gather, group_info=b[0].data_ptr(), step_rec=b[1].data_ptr(),
+            coef_tab=b[2].data_ptr(), gather_ptr=b[3].data_ptr(), gather_ent=b[4].data_ptr(),
+            out_col=b[5].data_ptr(),
+        )
+
+
+class DeviceProgram:
+    """A compiled coupling program.  Two device schedules are derived from the
+    same couplings on demand: the 9-point fast path (stencil9_kernel) and the
+    general one (program_kernel)."""
+
+    def __init__(self, couplings, out_widths, n_inputs: int | None = None):
+        self.couplings = [c for c in couplings if c is not None]
+        self._widths = tuple(int(w) for w in out_widths)
+        self.n_inputs = n_inputs
+        self._generic = None
+        self._fast9 = None
+        self._fast9_tried = False
 
     @property
     def out_widths(self) -> tuple[int, ...]:
-        return self.host.out_widths
+        return self._widths
+
+    @property
+    def generic(self) -> _GenericProgram:
+        if self._generic is None:
+            self._generic = _GenericProgram(compile_program(self.couplings, self._widths, n_inputs=self.n_inputs))
+        return self._generic
+
+    @property
+    def fast9(self) -> _Program9 | None:
+        if not self._fast9_tried:
+            self._fast9_tried = True
+            host = compile_program9(self.couplings, self._widths, n_inputs=self.n_inputs)
+            self._fast9 = _Program9(host) if host is not None else None
+        return self._fast9
+
+    @property
+    def host(self):
+        """Schedule statistics of the path the fast kernel would run."""
+        f = self.fast9
+        return f.host if f is not None else self.generic.host
 
 
 def _view(t: torch.Tensor | None, col0: int = 0) -> _lib.View:
@@ -194,8 +264,19 @@ def run_program(
     init_arr = (_lib.View * n_out)(*[_view(*i) if i is not None else _view(None) for i in inits])
     a = (ctypes.c_double * n_out)(*(alpha or [1.0] * n_out))
     b = (ctypes.c_double * n_out)(*(beta or [1.0] * n_out))
-    rc = _lib.lib().sgk_program_apply(
-        ctypes.byref(pattern.struct), ctypes.byref(program.struct), len(inputs), in_arr, n_out,
+    lib = _lib.lib()
+    p9 = pattern.pattern9() if FAST9 else None
+    if p9 is not None and program.fast9 is not None:
+        h9 = program.fast9.host
+        chunks = (h9.n_out_cols + 31) // 32
+        warps = min(8, max(1, h9.n_groups, -(-chunks // 16)))
+        rc = lib.sgk_stencil9_apply(ctypes.byref(p9), ctypes.byref(program.fast9.struct), len(inputs), in_arr,
+                                    n_out, out_arr, init_arr, a, b, 32 * warps, _lib.stream_ptr(stream))
+        if rc != -3:  # -3: does not fit in shared memory -> general kernel
+            _lib.check(rc, "sgk_stencil9_apply")
+            return
+    rc = lib.sgk_program_apply(
+        ctypes.byref(pattern.struct), ctypes.byref(program.generic.struct), len(inputs), in_arr, n_out,
         out_arr, init_arr, a, b, threads, _lib.stream_ptr(stream),
     )
     _lib.check(rc, "sgk_program_apply")

@@ -140,7 +140,7 @@ class KroneckerSumOperator:
                 h = self.couplings[t].tocsr()
                 for src in src_ranges:
                     cps.append(coupling_from_csr(0, 0, t, h, src, dst, scale))
-            prog = DeviceProgram(compile_program(cps, (dst[1] - dst[0],), n_inputs=1))
+            prog = DeviceProgram(cps, (dst[1] - dst[0],), n_inputs=1)
             self._cache[key] = prog
         return prog
 
@@ -262,7 +262,7 @@ class SteadyKKT:
             cps.append(coupling_from_csr(1, 1, m, eye, full, full, self.beta))  # beta M U
             cps.append(coupling_from_csr(2, 1, m, eye, full, full, 1.0))  # M L
             cps.append(coupling_from_csr(1, 2, m, eye, full, full, 1.0))  # M U
-            prog = DeviceProgram(compile_program(cps, (n_xi, n_xi, n_xi), n_inputs=3))
+            prog = DeviceProgram(cps, (n_xi, n_xi, n_xi), n_inputs=3)
             self._cache["kkt_prog"] = prog
         return prog
 

@@ -276,7 +276,7 @@ class SteadyKKTPreconditioner:
             n_xi = sys.n_xi
             w = sys.triple.objective_weight.tocsr()
             cp = coupling_from_csr(0, 0, sys.mass_slice, w, (0, n_xi), (0, n_xi), 1.0)
-            prog = DeviceProgram(compile_program([cp], (n_xi,), n_inputs=1))
+            prog = DeviceProgram([cp], (n_xi,), n_inputs=1)
             self._cache["wm"] = prog
         return prog
 
@@ -365,7 +365,7 @@ class CoupledSweepPreconditioner:
             cps.append(coupling_from_csr(2, 1, m, ident, src, dst, -1.0))
             cps.append(coupling_from_csr(1, 2, m, ident, src, dst, -1.0))
         w = dst[1] - dst[0]
-        return DeviceProgram(compile_program(cps, (w, w, w), n_inputs=3))
+        return DeviceProgram(cps, (w, w, w), n_inputs=3)
 
     def _programs(self):
         progs = self._cache.get("progs")

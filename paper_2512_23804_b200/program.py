@@ -347,3 +347,143 @@ def emulate(prog: HostProgram, pattern_rowptr, pattern_colind, slice_vals_std, i
         outs.append(y)
         off += w
     return outs
+
+
+@dataclass
+class HostProgram9:
+    """Contiguous-group uniform schedule for the 9-point fast path
+    (csrc/stencil9.cu; layout documented in include/sgkkt_b200.h)."""
+
+    n_groups: int
+    n_steps: int
+    n_ubuf: int
+    n_out_cols: int
+    n_coef: int
+    n_gather: int
+    group_info: np.ndarray
+    step_rec: np.ndarray
+    coef_tab: np.ndarray
+    gather_ptr: np.ndarray
+    gather_ent: np.ndarray
+    out_col: np.ndarray
+    out_widths: tuple[int, ...]
+    stats: dict = field(default_factory=dict)
+
+
+GROUP_COLS = 128  # 4 column slots x 32 lanes
+
+
+def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | None = None) -> HostProgram9 | None:
+    """Schedule for stencil9_kernel, or None when the gather does not fit its
+    packed encoding (> 16384 distinct coefficients)."""
+    out_widths = tuple(int(w) for w in out_widths)
+    couplings = [c for c in couplings if c is not None and len(c.rows)]
+    out_off = np.concatenate([[0], np.cumsum(out_widths)]).astype(np.int64)
+    n_out_cols = int(out_off[-1])
+    if couplings:
+        s_arr = np.concatenate([np.full(len(c.rows), c.s, np.int64) for c in couplings])
+        t_arr = np.concatenate([np.full(len(c.rows), c.t, np.int64) for c in couplings])
+        l_arr = np.concatenate([np.asarray(c.rows, np.int64) for c in couplings])
+        o_arr = np.concatenate([np.full(len(c.rows), c.o, np.int64) for c in couplings])
+        k_arr = np.concatenate([np.asarray(c.cols, np.int64) for c in couplings])
+        v_arr = np.concatenate([np.asarray(c.vals, np.float64) for c in couplings])
+    else:
+        s_arr = t_arr = l_arr = o_arr = k_arr = np.zeros(0, np.int64)
+        v_arr = np.zeros(0)
+    coef_tab, coef_idx = np.unique(v_arr, return_inverse=True)
+    if len(coef_tab) == 0:
+        coef_tab = np.zeros(1)
+    if len(coef_tab) > (1 << 14):
+        return None
+    # groups of 128 consecutive columns per input (the last one shifted left so
+    # it stays 128 wide when the input spans >= 128 columns: a column covered
+    # twice is computed twice, its product slot is taken from the first group)
+    group_info = []
+    step_rec = []
+    slot_of = {}  # (s, l, t) -> slot
+    n_ubuf = 0
+    executed = 0
+    for s in np.unique(s_arr):
+        sel = s_arr == s
+        cols = np.unique(l_arr[sel])
+        ts_s, ls_s = t_arr[sel], l_arr[sel]
+        span_hi = int(cols[-1]) + 1
+        i = 0
+        while i < len(cols):
+            col0 = int(cols[i])
+            j = int(np.searchsorted(cols, col0 + GROUP_COLS))
+            if span_hi >= GROUP_COLS:
+                col0 = min(col0, span_hi - GROUP_COLS)
+                ncols = GROUP_COLS
+            else:
+                ncols = span_hi - col0
+            in_g = (ls_s >= col0) & (ls_s < col0 + ncols)
+            gt, gl = ts_s[in_g], ls_s[in_g] - col0
+            q0 = len(step_rec)
+            group_info.append((int(s), col0, ncols, q0))
+            for qq, t in enumerate(np.unique(gt)):
+                step_rec.append(int(t))
+                for l in np.unique(gl[gt == t]):
+                    key = (int(s), col0 + int(l), int(t))
+                    if key not in slot_of:
+                        lane, c = int(l) % 32, int(l) // 32
+                        slot_of[key] = n_ubuf + qq * GROUP_COLS + lane * 4 + c
+                executed += GROUP_COLS
+            n_ubuf += GROUP_COLS * (len(step_rec) - q0)
+            i = j
+    n_steps = len(step_rec)
+    group_info.append((0, 0, 0, n_steps))
+    zero = n_ubuf + 32  # 32 zero slots after 32 spare slots
+    n_ent = len(v_arr)
+    slots = np.array([slot_of[(int(a), int(b), int(c))] for a, b, c in zip(s_arr, l_arr, t_arr)], dtype=np.int64)
+    c_arr = out_off[o_arr] + k_arr if n_ent else np.zeros(0, np.int64)
+    ordr = np.lexsort((l_arr, t_arr, c_arr)) if n_ent else np.zeros(0, np.int64)
+    counts = np.bincount(c_arr, minlength=n_out_cols) if n_ent else np.zeros(n_out_cols, np.int64)
+    starts = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    packed = (slots[ordr].astype(np.uint64) << np.uint64(14)) | coef_idx[ordr].astype(np.uint64) if n_ent else np.zeros(0, np.uint64)
+    # SELL-32: positions sorted by entry count so a warp's lanes have similar trip counts
+    pos_cols = np.argsort(-counts, kind="stable")
+    n_chunks = (n_out_cols + 31) // 32
+    pad_word = np.uint64(zero << 14)
+    chunk_meta = []
+    ents = []
+    off = 0
+    out_col = -np.ones(n_chunks * 32, np.int64)
+    o_of_c = np.repeat(np.arange(len(out_widths)), out_widths)
+    k_of_c = np.concatenate([np.arange(w) for w in out_widths]) if n_out_cols else np.zeros(0, np.int64)
+    for ch in range(n_chunks):
+        cols_ch = pos_cols[32 * ch : 32 * ch + 32]
+        cnt = int(counts[cols_ch].max()) if len(cols_ch) else 0
+        block = np.full((cnt, 32), pad_word, dtype=np.uint64)
+        for lane, c in enumerate(cols_ch):
+            e = packed[starts[c]:starts[c + 1]]
+            block[: len(e), lane] = e
+            out_col[32 * ch + lane] = (int(o_of_c[c]) << 24) | int(k_of_c[c])
+        chunk_meta.append((cnt, off))
+        ents.append(block.reshape(-1))
+        off += cnt * 32
+    gather_ptr = np.array(chunk_meta, dtype=np.int64).reshape(-1) if chunk_meta else np.zeros(2, np.int64)
+    ent = np.concatenate(ents) if ents else np.zeros(0, np.uint64)
+    n_gather = int(len(ent))
+    useful = len(slot_of)
+    stats = {"mode": "stencil9", "n_products": int(useful), "n_groups": len(group_info) - 1,
+             "n_steps": n_steps, "lane_efficiency": float(useful / executed) if executed else 1.0,
+             "n_gather": int(n_ent), "n_gather_padded": n_gather, "n_ubuf": int(n_ubuf),
+             "n_coef": int(len(coef_tab))}
+    i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
+    return HostProgram9(
+        n_groups=len(group_info) - 1,
+        n_steps=n_steps,
+        n_ubuf=int(n_ubuf),
+        n_out_cols=n_out_cols,
+        n_coef=int(len(coef_tab)),
+        n_gather=n_gather,
+        group_info=i32(np.array(group_info, dtype=np.int64).reshape(-1)),
+        step_rec=i32(np.array(step_rec, dtype=np.int64) if step_rec else np.zeros(1)),
+        coef_tab=np.ascontiguousarray(coef_tab if len(coef_tab) else np.zeros(1)),
+        gather_ptr=i32(gather_ptr),
+        gather_ent=np.ascontiguousarray(ent.astype(np.uint32) if n_gather else np.zeros(1, np.uint32)),
+        out_col=i32(out_col if n_out_cols else -np.ones(1)),
+        out_widths=out_widths,
+        stats=stats,
+    )
