@@ -151,7 +151,7 @@ typedef struct {
   const double* vals;
   const double* diag_inv; /* [n] or NULL                                   */
   const int32_t* order;   /* [n] topological (level) order                */
-  int32_t* flags;         /* [n] scratch, zero-initialised once            */
+  int32_t* flags;         /* [n * ceil(width/CW)] scratch, zeroed once     */
   int32_t* ticket;        /* [1] scratch                                   */
 } sgk_trifactor;
 
@@ -167,6 +167,8 @@ typedef struct {
  * in_perm[k]  = source row of B for factor row k   (inverse of perm_r)
  * out_perm[k] = destination row of X for factor row k (inverse of perm_c)
  * work: n x width contiguous scratch.  B and X may alias.                   */
+/* CW: RHS columns per solve task (flags are per (row, CW-column chunk)).   */
+int32_t sgk_trisolve_chunk_cols(void);
 int sgk_trisolve(const sgk_trifactor* L, const sgk_trifactor* U,
                  const int32_t* in_perm, const int32_t* out_perm,
                  const sgk_segview* b, const sgk_segview* x, double* work,

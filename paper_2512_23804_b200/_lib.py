@@ -113,6 +113,7 @@ _SIGNATURES = {
     "sgk_trisolve": (c_i32, [ctypes.POINTER(TriFactor), ctypes.POINTER(TriFactor), c_vp, c_vp,
                              ctypes.POINTER(SegView), ctypes.POINTER(SegView), c_vp, c_i32,
                              c_i32, c_vp]),
+    "sgk_trisolve_chunk_cols": (c_i32, []),
     "sgk_cheb_step": (c_i32, [ctypes.POINTER(Pattern), c_i32, c_vp, c_i64, c_vp, c_vp, c_vp,
                               c_vp, c_dbl, c_vp]),
     "sgk_colscale": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_i32, c_dbl, c_vp, c_vp]),

@@ -133,6 +133,18 @@ class TriangularFactors:
                    nnz_u=int(u_strict.nnz), bufs=bufs, l_struct=l_struct, u_struct=u_struct,
                    in_perm=_i32(in_perm), out_perm=_i32(out_perm))
 
+    def _ensure_flags(self, width: int) -> None:
+        """Readiness flags per (row, 16-column chunk); grown on demand."""
+        chunks = -(-width // int(_lib.lib().sgk_trisolve_chunk_cols()))
+        if chunks <= getattr(self, "_flag_chunks", 0):
+            return
+        dev = self.in_perm.device
+        self._flags_l = torch.zeros(max(self.n, 1) * chunks, dtype=torch.int32, device=dev)
+        self._flags_u = torch.zeros(max(self.n, 1) * chunks, dtype=torch.int32, device=dev)
+        self.l_struct.flags = self._flags_l.data_ptr()
+        self.u_struct.flags = self._flags_u.data_ptr()
+        self._flag_chunks = chunks
+
     def solve_segments(self, b_segs: list[tuple[torch.Tensor, int]], x_segs: list[tuple[torch.Tensor, int]],
                        width: int, stream=None) -> None:
         """x = A^-1 b on `width` columns of (up to 3) row segments that stack
@@ -162,6 +174,7 @@ class TriangularFactors:
         bv = segview(b_segs)
         xv = segview(x_segs)
         work = torch.empty((self.n, width), dtype=torch.float64, device=b_segs[0][0].device)
+        self._ensure_flags(width)
         self.epoch += 1
         rc = _lib.lib().sgk_trisolve(
             ctypes.byref(self.l_struct), ctypes.byref(self.u_struct), self.in_perm.data_ptr(),
