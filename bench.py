@@ -138,6 +138,25 @@ def cpu_sample(bundle, x, budget_s=3.0):
     return b / dt / 1e9, dt, rows, b
 
 
+def reduce_max(value: float, device=None) -> float:
+    """Max over ranks (the contract's "max over ranks" timing); identity when
+    not distributed.  NCCL on the GPU path, gloo in the CPU tests."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_gbs(bytes_per_step: int, steps: int, world: int, seconds_max: float) -> float:
+    """Weak scaling: every rank runs its own `steps` matvecs; the job's
+    throughput is all ranks' bytes over the slowest rank's time."""
+    return world * steps * bytes_per_step / seconds_max / 1e9
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -313,12 +332,10 @@ def run_ours(args):
         t = _event_time(step, args.steps, stream)
     launches = _lib.launch_count() - l0
     torch.cuda.synchronize()
+    t = reduce_max(t, dev)
     if ws > 1:
-        tt = torch.tensor([t], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
         dist.barrier()
-    value = ws * args.steps * B / t / 1e9
+    value = whole_job_gbs(B, args.steps, ws, t)
     kernel_avg = t / args.steps
 
     # e2e through the public API with pinned host buffers
@@ -338,11 +355,8 @@ def run_ours(args):
     ev1.synchronize()
     t_e2e = ev0.elapsed_time(ev1) / 1e3
     e2e_err = float(np.abs(wp.numpy() - w.cpu().numpy()).max())
-    if ws > 1:
-        tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
-    e2e_value = ws * e2e_steps * B / t_e2e / 1e9
+    t_e2e = reduce_max(t_e2e, dev)
+    e2e_value = whole_job_gbs(B, e2e_steps, ws, t_e2e)
 
     peak, peak_kind = _peaks()
     achieved = B / kernel_avg / 1e9

@@ -487,3 +487,43 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
         out_widths=out_widths,
         stats=stats,
     )
+
+
+def emulate9(prog: HostProgram9, mats, inputs, inits, alpha, beta):
+    """NumPy emulation of stencil9_kernel's schedule (test helper): mats[t]
+    is slice t as a SciPy matrix, inputs[s] the (n, width) input arrays."""
+    n_rows = mats[0].shape[0]
+    ub = np.zeros((n_rows, prog.n_ubuf + 64))
+    gi = prog.group_info.reshape(-1, 4)
+    base = 0
+    for g in range(prog.n_groups):
+        s, col0, ncols, q0 = (int(v) for v in gi[g])
+        q1 = int(gi[g + 1, 3])
+        x = inputs[s]
+        for q in range(q0, q1):
+            t = int(prog.step_rec[q])
+            for c in range(4):
+                for lane in range(32):
+                    col = col0 + min(32 * c + lane, ncols - 1)
+                    ub[:, base + (q - q0) * GROUP_COLS + lane * 4 + c] = mats[t] @ x[:, col]
+        base += GROUP_COLS * (q1 - q0)
+    n_chunks = (prog.n_out_cols + 31) // 32
+    meta = prog.gather_ptr.reshape(-1, 2)
+    acc = np.zeros((n_rows, n_chunks * 32))
+    for ch in range(n_chunks):
+        cnt, off = int(meta[ch, 0]), int(meta[ch, 1])
+        for e in range(cnt):
+            for lane in range(32):
+                w = int(prog.gather_ent[off + e * 32 + lane])
+                acc[:, ch * 32 + lane] += prog.coef_tab[w & 0x3FFF] * ub[:, w >> 14]
+    outs = [np.zeros((n_rows, w)) for w in prog.out_widths]
+    for pos in range(n_chunks * 32):
+        oc = int(prog.out_col[pos])
+        if oc < 0:
+            continue
+        o, k = oc >> 24, oc & 0xFFFFFF
+        y = alpha[o] * acc[:, pos]
+        if inits[o] is not None:
+            y = y + beta[o] * inits[o][:, k]
+        outs[o][:, k] = y
+    return outs

@@ -1,0 +1,44 @@
+"""The N>1 bench plumbing on CPU with gloo, world_size 2: max-over-ranks
+timing and the weak-scaling whole-job value; the reference arm prints only
+on rank 0."""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+
+    t = bench.reduce_max(1.0 + rank)
+    out[rank] = (t, bench.whole_job_gbs(1_000_000_000, 10, world, t))
+    dist.destroy_process_group()
+
+
+def test_reduce_max_and_weak_scaling_gloo():
+    port = 29500 + os.getpid() % 1000
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0][0] == 2.0 and out[1][0] == 2.0
+    assert abs(out[0][1] - 2 * 10 * 1.0 / 2.0) < 1e-12  # 2 ranks x 10 GB / 2 s
+
+
+def test_reference_arm_nonzero_rank_is_silent():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="1", LOCAL_RANK="1")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1"],
+                       capture_output=True, text=True, env=env, cwd=ROOT, timeout=120)
+    assert r.returncode == 0
+    assert r.stdout.strip() == ""
