@@ -155,6 +155,30 @@ typedef struct {
   int32_t* ticket;        /* [1] scratch                                   */
 } sgk_trifactor;
 
+/* Grouped (chain-supernodal) triangle in "processing space": rows in
+ * dependency order, strictly lower CSR; consecutive rows that each depend on
+ * the previous one form a group of <= 32 rows solved by one CTA without a
+ * global round trip per row.  L is passed as is (work_row[p] = p, io_row[p] =
+ * source row of b, diag_inv = NULL); U is passed reversed (p = n-1-k,
+ * work_row[p] = k, io_row[p] = destination row of x, diag_inv[p] = 1/U_kk).  */
+typedef struct {
+  int32_t n;
+  int32_t n_groups;
+  int32_t reversed;           /* 0: work_row[p] == p, 1: == n-1-p          */
+  int32_t pad;
+  const int32_t* rowptr;      /* [n+1]                                     */
+  const int32_t* split;       /* [n] first entry of row p inside its group */
+  const int32_t* colind;      /* processing-space columns, sorted          */
+  const double* vals;
+  const int32_t* group_ptr;   /* [n_groups+1] row ranges                   */
+  const int32_t* group_order; /* [n_groups] topological (level) order      */
+  const int32_t* work_row;    /* [n]                                       */
+  const int32_t* io_row;      /* [n]                                       */
+  const double* diag_inv;     /* [n] or NULL                               */
+  int32_t* flags;             /* [n * ceil(width/CW)] scratch              */
+  int32_t* ticket;            /* [1] scratch                               */
+} sgk_trigroups;
+
 /* Segmented row view: global row r lives in segment r / seg_rows.          */
 typedef struct {
   double* ptr[3];
@@ -173,6 +197,13 @@ int sgk_trisolve(const sgk_trifactor* L, const sgk_trifactor* U,
                  const int32_t* in_perm, const int32_t* out_perm,
                  const sgk_segview* b, const sgk_segview* x, double* work,
                  int32_t width, int32_t epoch, void* stream);
+
+/* Same result as sgk_trisolve, grouped task granularity (flags per
+ * (row, sgk_trisolve_grouped_chunk_cols()-column chunk)).                   */
+int32_t sgk_trisolve_grouped_chunk_cols(void);
+int sgk_trisolve_grouped(const sgk_trigroups* L, const sgk_trigroups* U,
+                         const sgk_segview* b, const sgk_segview* x,
+                         double* work, int32_t width, int32_t epoch, void* stream);
 
 /* One Chebyshev semi-iteration step on all columns (preconditioners.py:89-97):
  * x_new = omega*(scale .* (b - M x) + x - x_prev) + x_prev,

@@ -96,6 +96,14 @@ class TriFactor(ctypes.Structure):
     ]
 
 
+class TriGroups(ctypes.Structure):
+    _fields_ = [
+        ("n", c_i32), ("n_groups", c_i32), ("reversed", c_i32), ("pad", c_i32), ("rowptr", c_vp), ("split", c_vp), ("colind", c_vp), ("vals", c_vp),
+        ("group_ptr", c_vp), ("group_order", c_vp), ("work_row", c_vp), ("io_row", c_vp),
+        ("diag_inv", c_vp), ("flags", c_vp), ("ticket", c_vp),
+    ]
+
+
 class SegView(ctypes.Structure):
     _fields_ = [("ptr", c_vp * 3), ("ld", c_i64), ("col0", c_i32), ("seg_rows", c_i32)]
 
@@ -114,6 +122,10 @@ _SIGNATURES = {
                              ctypes.POINTER(SegView), ctypes.POINTER(SegView), c_vp, c_i32,
                              c_i32, c_vp]),
     "sgk_trisolve_chunk_cols": (c_i32, []),
+    "sgk_trisolve_grouped_chunk_cols": (c_i32, []),
+    "sgk_trisolve_grouped": (c_i32, [ctypes.POINTER(TriGroups), ctypes.POINTER(TriGroups),
+                                     ctypes.POINTER(SegView), ctypes.POINTER(SegView), c_vp, c_i32, c_i32,
+                                     c_vp]),
     "sgk_cheb_step": (c_i32, [ctypes.POINTER(Pattern), c_i32, c_vp, c_i64, c_vp, c_vp, c_vp,
                               c_vp, c_dbl, c_vp]),
     "sgk_colscale": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_i32, c_dbl, c_vp, c_vp]),

@@ -18,6 +18,8 @@
 //     partial sums, then a butterfly reduction over the warp;
 //   wide: lanes split the columns, entries processed 8 at a time with all 8
 //     loads in flight.
+#include <algorithm>
+
 #include "sgk_common.cuh"
 
 namespace sgk {
@@ -149,9 +151,198 @@ static int launch_chunked(const sgk_trifactor& L, const sgk_trifactor& U, const 
   return check_launch("trsv_chunk<bwd>");
 }
 
+// ---------------------------------------------------------------------------
+// Grouped (chain-supernodal) solve.  Consecutive factor rows where each row
+// depends on the previous one form a group (<= 32 rows); a task is (group,
+// 16-column chunk) and is run by one CTA:
+//   0. wait for every dependency outside the group (flags polled relaxed in
+//      batches, one acquire fence);
+//   1. outside contributions of all rows of the group in parallel (warps over
+//      rows, lanes over entries, all loads of a batch in flight);
+//   2. the in-group chain solved by one warp from shared memory (no global
+//      round trip per row — the reason for grouping: the COLAMD factors'
+//      critical path is mostly such chains);
+//   3. results written, fenced, group flags published.
+// The triangle is given in "processing space" (rows in dependency order,
+// strictly lower); the U factor is passed reversed.
+constexpr int GMAX = 32;
+constexpr int GEPL = 4;
+constexpr int GCW = 8;  // RHS columns per grouped task
+
+template <bool FWD>
+__global__ void __launch_bounds__(256) trsv_group(sgk_trigroups t, sgk_segview io, double* __restrict__ work,
+                                                  int width, int n_chunks, int epoch) {
+  __shared__ double part[GMAX][GCW];
+  __shared__ double ys[GMAX][GCW];
+  __shared__ double lg[GMAX][GMAX + 1];  // dense in-group block (strictly lower)
+  __shared__ int task_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const int64_t n_tasks = (int64_t)t.n_groups * n_chunks;
+  for (;;) {
+    if (tid == 0) task_s = atomicAdd(t.ticket, 1);
+    __syncthreads();
+    const int ticket = task_s;
+    __syncthreads();
+    if (ticket >= n_tasks) return;
+    const int gi = __ldg(t.group_order + ticket / n_chunks);
+    const int chunk = ticket - (ticket / n_chunks) * n_chunks;
+    const int r0 = __ldg(t.group_ptr + gi), r1 = __ldg(t.group_ptr + gi + 1);
+    const int g = r1 - r0;
+    const int c0 = chunk * GCW;
+    const int w = min(GCW, width - c0);
+
+    // 0: wait for every outside dependency of the whole group at once (the
+    //    group's rows are contiguous in CSR; all polls of a thread in flight)
+    {
+      const int ea = __ldg(t.rowptr + r0), eb = __ldg(t.rowptr + r1);
+      for (int base = ea; base < eb; base += 4 * blockDim.x) {
+        int cj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = base + tid + u * blockDim.x;
+          const int c = e < eb ? __ldg(t.colind + e) : -1;
+          cj[u] = c < r0 ? c : -1;
+        }
+        for (;;) {
+          bool ready = true;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (cj[u] >= 0) ready &= ld_relaxed(t.flags + (int64_t)cj[u] * n_chunks + chunk) == epoch;
+          if (ready) break;
+          __nanosleep(64);
+        }
+      }
+      fence_acq_rel();
+    }
+    __syncthreads();
+
+    // 1: outside contributions, rows over warps (all dependencies ready)
+    for (int r = warp; r < g; r += nwarps) {
+      const int p = r0 + r;
+      const int e0 = __ldg(t.rowptr + p), e2 = __ldg(t.rowptr + p + 1);
+      const int e1 = __ldg(t.split + p);  // first in-group entry (host-computed)
+      lg[r][lane] = 0.0;
+      __syncwarp();
+      if (lane < e2 - e1) lg[r][__ldg(t.colind + e1 + lane) - r0] = __ldg(t.vals + e1 + lane);
+      double acc[GCW];
+#pragma unroll
+      for (int c = 0; c < GCW; ++c) acc[c] = 0.0;
+      for (int base = e0; base < e1; base += 32 * GEPL) {
+        int cj[GEPL];
+        double vj[GEPL];
+#pragma unroll
+        for (int u = 0; u < GEPL; ++u) {
+          const int e = base + lane + 32 * u;
+          const int c = e < e1 ? __ldg(t.colind + e) : -1;
+          cj[u] = c;
+          vj[u] = c >= 0 ? __ldg(t.vals + e) : 0.0;
+        }
+        double xv[GEPL][GCW];
+#pragma unroll
+        for (int u = 0; u < GEPL; ++u) {
+          const int wr = t.reversed ? t.n - 1 - max(cj[u], 0) : max(cj[u], 0);
+          const double* zr = work + (int64_t)wr * width + c0;
+#pragma unroll
+          for (int c = 0; c < GCW; ++c) xv[u][c] = (cj[u] >= 0 && c < w) ? __ldcg(zr + c) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < GEPL; ++u)
+#pragma unroll
+          for (int c = 0; c < GCW; ++c) acc[c] = fma(-vj[u], xv[u][c], acc[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < GCW; ++c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(FULL, acc[c], o);
+      }
+      if (lane < w) {
+        double s = acc[0];
+#pragma unroll
+        for (int c = 1; c < GCW; ++c)
+          if (lane == c) s = acc[c];
+        const double init = FWD ? seg_load(io, __ldg(t.io_row + p), c0 + lane)
+                                : __ldcg(work + (int64_t)__ldg(t.work_row + p) * width + c0 + lane);
+        part[r][lane] = init + s;
+      }
+    }
+    __syncthreads();
+
+    // 2: the in-group chain, one warp, right-looking: lane r holds row r's
+    //    partial sums; after row j is final its values are broadcast and every
+    //    later row subtracts L[r][j] * y_j (no global traffic, no barrier)
+    if (warp == 0) {
+      double pr[GCW];
+      const bool mine = lane < g;
+#pragma unroll
+      for (int c = 0; c < GCW; ++c) pr[c] = mine ? part[lane][c] : 0.0;
+      const double d = (!FWD && mine) ? __ldg(t.diag_inv + r0 + lane) : 1.0;
+      for (int j = 0; j < g; ++j) {
+        const double l = (lane > j && mine) ? lg[lane][j] : 0.0;
+#pragma unroll
+        for (int c = 0; c < GCW; ++c) {
+          const double yj = __shfl_sync(FULL, pr[c] * d, j);
+          if (lane == j) ys[j][c] = yj;
+          pr[c] = fma(-l, yj, pr[c]);
+        }
+      }
+    }
+    __syncthreads();
+
+    // 3: write back, fence, publish
+    for (int i = tid; i < g * GCW; i += blockDim.x) {
+      const int r = i / GCW, c = i - r * GCW;
+      if (c < w) {
+        const int p = r0 + r;
+        __stcg(work + (int64_t)__ldg(t.work_row + p) * width + c0 + c, ys[r][c]);
+        if (!FWD) seg_store(io, __ldg(t.io_row + p), c0 + c, ys[r][c]);
+      }
+    }
+    fence_acq_rel();
+    __syncthreads();
+    if (tid < g) st_relaxed(t.flags + (int64_t)(r0 + tid) * n_chunks + chunk, epoch);
+  }
+}
+
+static int launch_grouped(const sgk_trigroups& L, const sgk_trigroups& U, const sgk_segview& b,
+                          const sgk_segview& x, double* work, int width, int n_chunks, int epoch,
+                          cudaStream_t st) {
+  const int threads = 256;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_group<true>, threads, 0);
+  if (occ < 1) occ = 1;
+  if (occ > 2) occ = 2;
+  int64_t grid = (int64_t)sm_count() * occ;
+  const int64_t tasks = (int64_t)std::max(L.n_groups, U.n_groups) * n_chunks;
+  if (grid > tasks) grid = tasks;
+  if (grid < 1) grid = 1;
+  cudaMemsetAsync(L.ticket, 0, sizeof(int32_t), st);
+  cudaMemsetAsync(U.ticket, 0, sizeof(int32_t), st);
+  trsv_group<true><<<(int)grid, threads, 0, st>>>(L, b, work, width, n_chunks, epoch);
+  int rc = check_launch("trsv_group<fwd>");
+  if (rc) return rc;
+  trsv_group<false><<<(int)grid, threads, 0, st>>>(U, x, work, width, n_chunks, epoch);
+  return check_launch("trsv_group<bwd>");
+}
+
 }  // namespace sgk
 
+extern "C" int sgk_trisolve_grouped(const sgk_trigroups* L, const sgk_trigroups* U, const sgk_segview* b,
+                                    const sgk_segview* x, double* work, int32_t width, int32_t epoch,
+                                    void* stream) {
+  using namespace sgk;
+  SGK_REQUIRE(L && U && b && x && work, "sgk_trisolve_grouped: null argument");
+  SGK_REQUIRE(L->n == U->n && L->n >= 0, "sgk_trisolve_grouped: factor sizes differ");
+  SGK_REQUIRE(U->diag_inv != nullptr && L->diag_inv == nullptr, "sgk_trisolve_grouped: expected unit L, U with diag");
+  SGK_REQUIRE(width >= 0 && epoch > 0, "sgk_trisolve_grouped: bad width/epoch");
+  SGK_REQUIRE(b->seg_rows > 0 && x->seg_rows > 0, "sgk_trisolve_grouped: seg_rows must be positive");
+  if (L->n == 0 || width == 0) return SGK_OK;
+  const int n_chunks = (width + GCW - 1) / GCW;
+  return launch_grouped(*L, *U, *b, *x, work, width, n_chunks, epoch, (cudaStream_t)stream);
+}
+
 extern "C" int32_t sgk_trisolve_chunk_cols(void) { return sgk::CW; }
+extern "C" int32_t sgk_trisolve_grouped_chunk_cols(void) { return sgk::GCW; }
 
 extern "C" int sgk_trisolve(const sgk_trifactor* L, const sgk_trifactor* U, const int32_t* in_perm,
                             const int32_t* out_perm, const sgk_segview* b, const sgk_segview* x,

@@ -77,6 +77,76 @@ def level_schedule(strict: csr_matrix, lower: bool) -> tuple[np.ndarray, int]:
     return order.astype(np.int64), depth
 
 
+GROUP_MAX = 32
+# SGKKT_TRISOLVE=rows selects the row-granular kernel (A/B testing)
+GROUPED = __import__("os").environ.get("SGKKT_TRISOLVE", "grouped") != "rows"
+
+
+def chain_groups(strict: csr_matrix, max_rows: int = GROUP_MAX) -> tuple[np.ndarray, np.ndarray, int]:
+    """Group consecutive rows of a strictly lower triangle into chains (row k
+    joins the group of row k-1 when it depends on row k-1), and order the
+    groups topologically by group level.  Returns (group_ptr, order, depth)."""
+    n = strict.shape[0]
+    ip, ix = strict.indptr, strict.indices
+    starts = [0]
+    for k in range(1, n):
+        dep_prev = ip[k + 1] > ip[k] and ix[ip[k + 1] - 1] == k - 1
+        if not dep_prev or k - starts[-1] >= max_rows:
+            starts.append(k)
+    gptr = np.array(starts + [n], dtype=np.int64) if n else np.zeros(1, np.int64)
+    ng = len(gptr) - 1
+    gid = np.repeat(np.arange(ng), np.diff(gptr))
+    level = np.zeros(ng, dtype=np.int64)
+    for g in range(ng):
+        a, b = gptr[g], gptr[g + 1]
+        cols = ix[ip[a]:ip[b]]
+        cols = cols[cols < a]
+        if cols.size:
+            level[g] = level[gid[cols]].max() + 1
+    order = np.argsort(level, kind="stable")
+    return gptr, order, int(level.max()) + 1 if ng else 0
+
+
+def grouped_triangles(l_strict, u_strict, diag, in_perm, out_perm):
+    """Processing-space triangles for sgk_trisolve_grouped: L as is, U
+    reversed (p = n-1-k) into a strictly lower triangle.  Returns
+    ((L, work_row, io_row, None), (U_rev, work_row, io_row, diag_inv))."""
+    n = l_strict.shape[0]
+    rev = np.arange(n)[::-1].copy()
+    pmat = sp.csr_matrix((np.ones(n), (np.arange(n), rev)), shape=(n, n))
+    u_rev = (pmat @ u_strict @ pmat).tocsr()
+    u_rev.sum_duplicates()
+    u_rev.sort_indices()
+    return (l_strict, np.arange(n), np.asarray(in_perm), None), (u_rev, rev, np.asarray(out_perm)[rev], 1.0 / diag[rev])
+
+
+def _grouped(strict: csr_matrix, work_row, io_row, dinv):
+    gptr, order, depth = chain_groups(strict)
+    n = strict.shape[0]
+    # first entry of each row whose column lies inside the row's own group
+    gstart = np.repeat(gptr[:-1], np.diff(gptr)) if n else np.zeros(0, np.int64)
+    row_of = np.repeat(np.arange(n), np.diff(strict.indptr))
+    inside = strict.indices >= gstart[row_of] if strict.nnz else np.zeros(0, bool)
+    split = strict.indptr[1:] - np.bincount(row_of[inside], minlength=n) if n else np.zeros(0, np.int64)
+    if n and np.any(np.diff(strict.indptr) - (strict.indptr[1:] - split) < 0):
+        raise AssertionError("bad group split")
+    dev = device()
+    bufs = [
+        _i32(strict.indptr), _i32(strict.indices if strict.nnz else [0]), _f64(strict.data if strict.nnz else [0.0]),
+        _i32(gptr), _i32(order if len(order) else [0]), _i32(work_row), _i32(io_row),
+        _f64(dinv) if dinv is not None else None, torch.zeros(1, dtype=torch.int32, device=dev),
+        _i32(split if n else [0]),
+    ]
+    st = _lib.TriGroups(
+        n=strict.shape[0], n_groups=len(gptr) - 1, reversed=int(n > 0 and work_row[0] != 0), pad=0, rowptr=bufs[0].data_ptr(), split=bufs[9].data_ptr(),
+        colind=bufs[1].data_ptr(),
+        vals=bufs[2].data_ptr(), group_ptr=bufs[3].data_ptr(), group_order=bufs[4].data_ptr(),
+        work_row=bufs[5].data_ptr(), io_row=bufs[6].data_ptr(),
+        diag_inv=bufs[7].data_ptr() if bufs[7] is not None else None, flags=None, ticket=bufs[8].data_ptr(),
+    )
+    return st, bufs, depth
+
+
 @dataclass(eq=False)
 class TriangularFactors:
     """Device copy of one SuperLU factorization."""
@@ -129,13 +199,18 @@ class TriangularFactors:
             vals=bufs[7].data_ptr(), diag_inv=bufs[10].data_ptr(), order=bufs[8].data_ptr(),
             flags=bufs[9].data_ptr(), ticket=ticket.data_ptr() + 4,
         )
-        return cls(n=n, depth_l=depth_l, depth_u=depth_u, nnz_l=int(l_strict.nnz),
-                   nnz_u=int(u_strict.nnz), bufs=bufs, l_struct=l_struct, u_struct=u_struct,
-                   in_perm=_i32(in_perm), out_perm=_i32(out_perm))
+        out = cls(n=n, depth_l=depth_l, depth_u=depth_u, nnz_l=int(l_strict.nnz),
+                  nnz_u=int(u_strict.nnz), bufs=bufs, l_struct=l_struct, u_struct=u_struct,
+                  in_perm=_i32(in_perm), out_perm=_i32(out_perm))
+        (lg, ug) = grouped_triangles(l_strict, u_strict, diag, in_perm, out_perm)
+        out.gl, out.gl_bufs, out.gdepth_l = _grouped(*lg)
+        out.gu, out.gu_bufs, out.gdepth_u = _grouped(*ug)
+        return out
 
     def _ensure_flags(self, width: int) -> None:
         """Readiness flags per (row, 16-column chunk); grown on demand."""
-        chunks = -(-width // int(_lib.lib().sgk_trisolve_chunk_cols()))
+        cw = min(int(_lib.lib().sgk_trisolve_chunk_cols()), int(_lib.lib().sgk_trisolve_grouped_chunk_cols()))
+        chunks = -(-width // cw)
         if chunks <= getattr(self, "_flag_chunks", 0):
             return
         dev = self.in_perm.device
@@ -143,6 +218,8 @@ class TriangularFactors:
         self._flags_u = torch.zeros(max(self.n, 1) * chunks, dtype=torch.int32, device=dev)
         self.l_struct.flags = self._flags_l.data_ptr()
         self.u_struct.flags = self._flags_u.data_ptr()
+        self.gl.flags = self._flags_l.data_ptr()
+        self.gu.flags = self._flags_u.data_ptr()
         self._flag_chunks = chunks
 
     def solve_segments(self, b_segs: list[tuple[torch.Tensor, int]], x_segs: list[tuple[torch.Tensor, int]],
@@ -176,6 +253,12 @@ class TriangularFactors:
         work = torch.empty((self.n, width), dtype=torch.float64, device=b_segs[0][0].device)
         self._ensure_flags(width)
         self.epoch += 1
+        if GROUPED:
+            rc = _lib.lib().sgk_trisolve_grouped(ctypes.byref(self.gl), ctypes.byref(self.gu), ctypes.byref(bv),
+                                                 ctypes.byref(xv), work.data_ptr(), width, self.epoch,
+                                                 _lib.stream_ptr(stream))
+            _lib.check(rc, "sgk_trisolve_grouped")
+            return
         rc = _lib.lib().sgk_trisolve(
             ctypes.byref(self.l_struct), ctypes.byref(self.u_struct), self.in_perm.data_ptr(),
             self.out_perm.data_ptr(), ctypes.byref(bv), ctypes.byref(xv), work.data_ptr(), width,

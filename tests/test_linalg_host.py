@@ -78,3 +78,60 @@ def test_csr_from_coo_validation():
         csr_from_coo(2, 2, [2], [0], [1.0])
     m = csr_from_coo(2, 2, [0, 0, 1], [1, 1, 0], [1.0, 2.0, 5.0])
     assert m[0, 1] == 3.0 and m.nnz == 2
+
+
+def emulate_grouped(lu, b):
+    """NumPy emulation of sgk_trisolve_grouped: group tasks in level order,
+    outside contributions first, then the in-group chain."""
+    from paper_2512_23804_b200.linalg import chain_groups, grouped_triangles
+
+    L = sp.tril(sp.csr_matrix(lu.L), k=-1, format="csr")
+    U = sp.csr_matrix(lu.U)
+    d = U.diagonal()
+    U = sp.triu(U, k=1, format="csr")
+    for m in (L, U):
+        m.sort_indices()
+    (lt, lw, lio, _), (ut, uw, uio, udinv) = grouped_triangles(L, U, d, np.argsort(lu.perm_r), np.argsort(lu.perm_c))
+    n = b.shape[0]
+    work = np.zeros_like(b)
+    x = np.zeros_like(b)
+    for tri, wrow, iorow, dinv, fwd in ((lt, lw, lio, None, True), (ut, uw, uio, udinv, False)):
+        gptr, order, _ = chain_groups(tri)
+        done = np.zeros(n, bool)
+        for g in order:
+            r0, r1 = gptr[g], gptr[g + 1]
+            part = {}
+            for p in range(r0, r1):
+                cols = tri.indices[tri.indptr[p]:tri.indptr[p + 1]]
+                vals = tri.data[tri.indptr[p]:tri.indptr[p + 1]]
+                out = cols < r0
+                assert done[cols[out]].all()
+                init = b[iorow[p]] if fwd else work[wrow[p]]
+                part[p] = init - vals[out] @ work[wrow[cols[out]]]
+            for p in range(r0, r1):
+                cols = tri.indices[tri.indptr[p]:tri.indptr[p + 1]]
+                vals = tri.data[tri.indptr[p]:tri.indptr[p + 1]]
+                inn = cols >= r0
+                y = part[p] - vals[inn] @ work[wrow[cols[inn]]]
+                if not fwd:
+                    y = y * dinv[p]
+                    x[iorow[p]] = y
+                work[wrow[p]] = y
+                done[p] = True
+    return x
+
+
+@pytest.mark.parametrize("kind", ["random", "kkt"])
+def test_grouped_trisolve_emulation(rng, kind):
+    if kind == "random":
+        a = sp.random(80, 80, density=0.08, random_state=5, format="csr") + 4 * sp.eye(80)
+    else:
+        b = build_problem(2, n=8)
+        s = steady_system(b)
+        a = sp.bmat([[s.mass, None, -s.stiffness[0]], [None, s.beta * s.mass, s.mass],
+                     [-s.stiffness[0], s.mass, None]], format="csr")
+    lu = spla.splu(sp.csc_matrix(a), diag_pivot_thresh=1.0)
+    rhs = rng.standard_normal((a.shape[0], 2))
+    want = lu.solve(rhs)
+    got = emulate_grouped(lu, rhs)
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
