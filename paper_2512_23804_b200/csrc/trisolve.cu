@@ -19,6 +19,7 @@
 //   wide: lanes split the columns, entries processed 8 at a time with all 8
 //     loads in flight.
 #include <algorithm>
+#include <cstdlib>
 
 #include "sgk_common.cuh"
 
@@ -166,11 +167,10 @@ static int launch_chunked(const sgk_trifactor& L, const sgk_trifactor& U, const 
 // The triangle is given in "processing space" (rows in dependency order,
 // strictly lower); the U factor is passed reversed.
 constexpr int GMAX = 32;
-constexpr int GEPL = 4;
-constexpr int GCW = 8;  // RHS columns per grouped task
+constexpr int GCW_MIN = 1;  // narrowest grouped chunk (sizes the flag array)
 
-template <bool FWD>
-__global__ void __launch_bounds__(256) trsv_group(sgk_trigroups t, sgk_segview io, double* __restrict__ work,
+template <bool FWD, int GCW, int GEPL>
+__global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview io, double* __restrict__ work,
                                                   int width, int n_chunks, int epoch) {
   __shared__ double part[GMAX][GCW];
   __shared__ double ys[GMAX][GCW];
@@ -304,25 +304,48 @@ __global__ void __launch_bounds__(256) trsv_group(sgk_trigroups t, sgk_segview i
   }
 }
 
-static int launch_grouped(const sgk_trigroups& L, const sgk_trigroups& U, const sgk_segview& b,
-                          const sgk_segview& x, double* work, int width, int n_chunks, int epoch,
-                          cudaStream_t st) {
-  const int threads = 256;
+template <int GCW, int GEPL>
+static int launch_grouped_t(const sgk_trigroups& L, const sgk_trigroups& U, const sgk_segview& b,
+                            const sgk_segview& x, double* work, int width, int epoch, int threads, int occ_cap,
+                            cudaStream_t st) {
+  const int n_chunks = (width + GCW - 1) / GCW;
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_group<true>, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_group<true, GCW, GEPL>, threads, 0);
   if (occ < 1) occ = 1;
-  if (occ > 2) occ = 2;
+  if (occ > occ_cap) occ = occ_cap;
   int64_t grid = (int64_t)sm_count() * occ;
   const int64_t tasks = (int64_t)std::max(L.n_groups, U.n_groups) * n_chunks;
   if (grid > tasks) grid = tasks;
   if (grid < 1) grid = 1;
   cudaMemsetAsync(L.ticket, 0, sizeof(int32_t), st);
   cudaMemsetAsync(U.ticket, 0, sizeof(int32_t), st);
-  trsv_group<true><<<(int)grid, threads, 0, st>>>(L, b, work, width, n_chunks, epoch);
+  trsv_group<true, GCW, GEPL><<<(int)grid, threads, 0, st>>>(L, b, work, width, n_chunks, epoch);
   int rc = check_launch("trsv_group<fwd>");
   if (rc) return rc;
-  trsv_group<false><<<(int)grid, threads, 0, st>>>(U, x, work, width, n_chunks, epoch);
+  trsv_group<false, GCW, GEPL><<<(int)grid, threads, 0, st>>>(U, x, work, width, n_chunks, epoch);
   return check_launch("trsv_group<bwd>");
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+static int launch_grouped(const sgk_trigroups& L, const sgk_trigroups& U, const sgk_segview& b,
+                          const sgk_segview& x, double* work, int width, int epoch, cudaStream_t st) {
+  // chunk width by RHS width (env overrides for tuning experiments)
+  // measured on B200 (tools/tri_sweep.py, profiles/r01_trisolve_sweep.txt):
+  // narrow chunks win up to ~40 columns, 4-column chunks above; 16 warps per task
+  int cw = env_int("SGKKT_TRI_CW", width <= 8 ? 1 : (width <= 40 ? 2 : 4));
+  const int threads = env_int("SGKKT_TRI_THREADS", 512);
+  const int occ_cap = env_int("SGKKT_TRI_OCC", 2);
+  const int epl = env_int("SGKKT_TRI_EPL", 8);
+  if (cw <= 1) return launch_grouped_t<1, 16>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
+  if (cw <= 2) return launch_grouped_t<2, 16>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
+  if (cw <= 4 && epl >= 16) return launch_grouped_t<4, 16>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
+  if (cw <= 4) return launch_grouped_t<4, 8>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
+  if (cw <= 8) return launch_grouped_t<8, 4>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
+  return launch_grouped_t<16, 2>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
 }
 
 }  // namespace sgk
@@ -337,12 +360,11 @@ extern "C" int sgk_trisolve_grouped(const sgk_trigroups* L, const sgk_trigroups*
   SGK_REQUIRE(width >= 0 && epoch > 0, "sgk_trisolve_grouped: bad width/epoch");
   SGK_REQUIRE(b->seg_rows > 0 && x->seg_rows > 0, "sgk_trisolve_grouped: seg_rows must be positive");
   if (L->n == 0 || width == 0) return SGK_OK;
-  const int n_chunks = (width + GCW - 1) / GCW;
-  return launch_grouped(*L, *U, *b, *x, work, width, n_chunks, epoch, (cudaStream_t)stream);
+  return launch_grouped(*L, *U, *b, *x, work, width, epoch, (cudaStream_t)stream);
 }
 
 extern "C" int32_t sgk_trisolve_chunk_cols(void) { return sgk::CW; }
-extern "C" int32_t sgk_trisolve_grouped_chunk_cols(void) { return sgk::GCW; }
+extern "C" int32_t sgk_trisolve_grouped_chunk_cols(void) { return sgk::GCW_MIN; }
 
 extern "C" int sgk_trisolve(const sgk_trifactor* L, const sgk_trifactor* U, const int32_t* in_perm,
                             const int32_t* out_perm, const sgk_segview* b, const sgk_segview* x,
