@@ -112,8 +112,11 @@ typedef struct {
  * sb3, 0, 0, 0} (inactive slots point at the 32 trash slots n_ubuf..);
  * gather in SELL-32 form: gather_ptr[2j], gather_ptr[2j+1] = entry count and
  * offset of chunk j (32 output positions), entries at off + e*32 + lane,
- * packed (slot << 14) | coef_index (padding reads the zero slots
- * n_ubuf+32..); out_col[position] = (output<<24)|column or -1.              */
+ * packed (ubuf byte offset << 14) | coef_tab byte offset, both relative to
+ * the kernel's dynamic shared memory (layout: coef_tab, 2 coefficient
+ * blocks, 2 column blocks, ubuf — so the program is compiled for the
+ * pattern's n_slices); padding reads the zero slots n_ubuf+32..;
+ * out_col[position] = (output<<24)|column or -1.                            */
 typedef struct {
   int32_t n_groups;
   int32_t n_steps;
@@ -121,6 +124,8 @@ typedef struct {
   int32_t n_out_cols;
   int32_t n_coef;
   int32_t n_gather;
+  int32_t n_slices;          /* pattern slices the entry offsets assume      */
+  int32_t pad;
   const int32_t* group_info; /* [(n_groups+1)*4]                            */
   const int32_t* step_rec;   /* [n_steps*8]                                 */
   const double* coef_tab;    /* [n_coef]                                    */

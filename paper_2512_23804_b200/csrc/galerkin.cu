@@ -162,6 +162,7 @@ static int launch_program_t(const sgk_pattern& pat, const sgk_program& prog, con
   if (!attr_set) {
     cudaFuncSetAttribute(program_kernel<MAXOUT, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
+    cudaGetLastError();
     attr_set = true;
   }
   int occ = 0;

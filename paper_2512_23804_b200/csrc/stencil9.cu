@@ -33,10 +33,10 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 __host__ __device__ inline Smem9 smem9_layout(int n_slices, const sgk_program9& p) {
   Smem9 s;
   size_t off = 0;
+  s.ctab = off;   off = align16(off + sizeof(double) * (size_t)p.n_coef);  // first: 14-bit offsets
   s.coef = off;   off = align16(off + 2 * sizeof(double) * (size_t)n_slices * 10);  // double buffer
   s.cols = off;   off = align16(off + 2 * 16 * sizeof(int32_t));
   s.ubuf = off;   off = align16(off + sizeof(double) * ((size_t)p.n_ubuf + 64));
-  s.ctab = off;   off = align16(off + sizeof(double) * (size_t)p.n_coef);
   s.steps = off;  off = align16(off + sizeof(int32_t) * (size_t)p.n_steps);
   s.groups = off; off = align16(off + sizeof(int32_t) * 4 * (size_t)(p.n_groups + 1));
   const size_t n_chunks = ((size_t)p.n_out_cols + 31) / 32;
@@ -91,6 +91,13 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
   const int warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
   const int n_chunks = (prog.n_out_cols + 31) >> 5;
+  __shared__ const double* in_ptr[SGK_MAX_IO];
+  __shared__ int64_t in_ld[SGK_MAX_IO];
+  if (tid < SGK_MAX_IO) {
+    const sgk_view& vv = pick(in, tid);
+    in_ptr[tid] = vv.ptr + vv.col0;
+    in_ld[tid] = vv.ld;
+  }
   const int ncoef = pat.n_slices * 10;
 
   // program tables -> shared memory, once per CTA
@@ -137,20 +144,21 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
     for (int g = warp; g < prog.n_groups; g += nwarps) {
       const int4 gi = *reinterpret_cast<const int4*>(groups + 4 * g);
       const int q1 = groups[4 * (g + 1) + 3];
-      const sgk_view& vv = pick(in, gi.x);
+      const double* vbase = in_ptr[gi.x] + gi.y;
+      const int64_t vld = in_ld[gi.x];
       double v[kCols][9];
       if (gi.z == 128) {
-        const double* base = vv.ptr + vv.col0 + gi.y + lane;
+        const double* base = vbase + lane;
 #pragma unroll
         for (int jj = 0; jj < 9; ++jj) {
-          const double* vr = base + (int64_t)cr[jj] * vv.ld;
+          const double* vr = base + cr[jj] * vld;
 #pragma unroll
           for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + 32 * c);
         }
       } else {
 #pragma unroll
         for (int jj = 0; jj < 9; ++jj) {
-          const double* vr = vv.ptr + (int64_t)cr[jj] * vv.ld + vv.col0 + gi.y;
+          const double* vr = vbase + cr[jj] * vld;
 #pragma unroll
           for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + min(32 * c + lane, gi.z - 1));
         }
@@ -181,9 +189,12 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
       const int cnt = ccnt[chunk];
       const uint32_t* ge = gent + coff[chunk] + lane;
       double acc = 0.0;
+      // entry = (ubuf byte offset << 14) | ctab byte offset, both relative to
+      // the dynamic shared-memory base
       for (int e = 0; e < cnt; ++e) {
         const uint32_t w = ge[32 * e];
-        acc = fma(ctab[w & 0x3FFF], ubuf[w >> 14], acc);
+        acc = fma(*reinterpret_cast<const double*>(sm + (w & 0x3FFF)),
+                  *reinterpret_cast<const double*>(sm + (w >> 14)), acc);
       }
       const int oc = ocol[r];
       if (oc >= 0) {
@@ -205,7 +216,14 @@ static int launch9(const sgk_pattern9& pat, const sgk_program9& prog, const View
   const Smem9 L = smem9_layout(pat.n_slices, prog);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(stencil9_kernel<MAXOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, stencil9_kernel<MAXOUT>);
+    cudaFuncSetAttribute(stencil9_kernel<MAXOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         optin - (int)fa.sharedSizeBytes);
+    cudaGetLastError();  // an attribute failure must not poison the launch check
     attr_set = true;
   }
   int occ = 0;
@@ -237,8 +255,8 @@ extern "C" int sgk_stencil9_apply(const sgk_pattern9* pat, const sgk_program9* p
   SGK_REQUIRE(n_in >= 0 && n_in <= SGK_MAX_IO && n_out >= 1 && n_out <= SGK_MAX_IO,
               "sgk_stencil9_apply: input/output count out of range");
   SGK_REQUIRE(prog->n_groups == 0 || n_in >= 1, "sgk_stencil9_apply: program needs inputs");
-  SGK_REQUIRE(prog->n_coef <= (1 << 14) && prog->n_ubuf <= (1 << 18),
-              "sgk_stencil9_apply: gather entry fields overflow");
+  SGK_REQUIRE((int64_t)prog->n_coef * 8 <= (1 << 14), "sgk_stencil9_apply: too many distinct coefficients");
+  SGK_REQUIRE(prog->n_slices == pat->n_slices, "sgk_stencil9_apply: program compiled for another slice count");
   const int threads = block_threads > 0 ? block_threads : 256;
   SGK_REQUIRE(threads % 32 == 0 && threads <= 256, "sgk_stencil9_apply: block_threads must be a multiple of 32, <=256");
   ViewSet vin{}, vout{}, vinit{};

@@ -185,7 +185,8 @@ class _Program9:
         b = self._bufs
         self.struct = _lib.Program9(
             n_groups=host.n_groups, n_steps=host.n_steps, n_ubuf=host.n_ubuf, n_out_cols=host.n_out_cols,
-            n_coef=host.n_coef, n_gather=host.n_gather, group_info=b[0].data_ptr(), step_rec=b[1].data_ptr(),
+            n_coef=host.n_coef, n_gather=host.n_gather, n_slices=host.n_slices, pad=0,
+            group_info=b[0].data_ptr(), step_rec=b[1].data_ptr(),
             coef_tab=b[2].data_ptr(), gather_ptr=b[3].data_ptr(), gather_ent=b[4].data_ptr(),
             out_col=b[5].data_ptr(),
         )
@@ -201,8 +202,7 @@ class DeviceProgram:
         self._widths = tuple(int(w) for w in out_widths)
         self.n_inputs = n_inputs
         self._generic = None
-        self._fast9 = None
-        self._fast9_tried = False
+        self._fast9 = {}
 
     @property
     def out_widths(self) -> tuple[int, ...]:
@@ -214,19 +214,21 @@ class DeviceProgram:
             self._generic = _GenericProgram(compile_program(self.couplings, self._widths, n_inputs=self.n_inputs))
         return self._generic
 
-    @property
-    def fast9(self) -> _Program9 | None:
-        if not self._fast9_tried:
-            self._fast9_tried = True
-            host = compile_program9(self.couplings, self._widths, n_inputs=self.n_inputs)
-            self._fast9 = _Program9(host) if host is not None else None
-        return self._fast9
+    def fast9(self, n_slices: int) -> _Program9 | None:
+        """9-point schedule for a pattern with `n_slices` value slices (the
+        gather entries encode shared-memory offsets that depend on it)."""
+        if n_slices not in self._fast9:
+            host = compile_program9(self.couplings, self._widths, n_inputs=self.n_inputs, n_slices_hint=n_slices)
+            self._fast9[n_slices] = _Program9(host) if host is not None else None
+        return self._fast9[n_slices]
 
     @property
     def host(self):
-        """Schedule statistics of the path the fast kernel would run."""
-        f = self.fast9
-        return f.host if f is not None else self.generic.host
+        """Schedule statistics of the fast path compiled last (else the general one)."""
+        for f in self._fast9.values():
+            if f is not None:
+                return f.host
+        return self.generic.host
 
 
 def _view(t: torch.Tensor | None, col0: int = 0) -> _lib.View:
@@ -266,11 +268,12 @@ def run_program(
     b = (ctypes.c_double * n_out)(*(beta or [1.0] * n_out))
     lib = _lib.lib()
     p9 = pattern.pattern9() if FAST9 else None
-    if p9 is not None and program.fast9 is not None:
-        h9 = program.fast9.host
+    f9 = program.fast9(pattern.n_slices) if p9 is not None else None
+    if f9 is not None:
+        h9 = f9.host
         chunks = (h9.n_out_cols + 31) // 32
         warps = min(8, max(1, h9.n_groups, -(-chunks // 16)))
-        rc = lib.sgk_stencil9_apply(ctypes.byref(p9), ctypes.byref(program.fast9.struct), len(inputs), in_arr,
+        rc = lib.sgk_stencil9_apply(ctypes.byref(p9), ctypes.byref(f9.struct), len(inputs), in_arr,
                                     n_out, out_arr, init_arr, a, b, 32 * warps, _lib.stream_ptr(stream))
         if rc != -3:  # -3: does not fit in shared memory -> general kernel
             _lib.check(rc, "sgk_stencil9_apply")

@@ -368,12 +368,14 @@ class HostProgram9:
     out_col: np.ndarray
     out_widths: tuple[int, ...]
     stats: dict = field(default_factory=dict)
+    n_slices: int = 0
 
 
 GROUP_COLS = 128  # 4 column slots x 32 lanes
 
 
-def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | None = None) -> HostProgram9 | None:
+def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | None = None,
+                     n_slices_hint: int | None = None) -> HostProgram9 | None:
     """Schedule for stencil9_kernel, or None when the gather does not fit its
     packed encoding (> 16384 distinct coefficients)."""
     out_widths = tuple(int(w) for w in out_widths)
@@ -393,7 +395,7 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
     coef_tab, coef_idx = np.unique(v_arr, return_inverse=True)
     if len(coef_tab) == 0:
         coef_tab = np.zeros(1)
-    if len(coef_tab) > (1 << 14):
+    if len(coef_tab) * 8 > (1 << 14):
         return None
     # groups of 128 consecutive columns per input (the last one shifted left so
     # it stays 128 wide when the input spans >= 128 columns: a column covered
@@ -434,17 +436,28 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
     n_steps = len(step_rec)
     group_info.append((0, 0, 0, n_steps))
     zero = n_ubuf + 32  # 32 zero slots after 32 spare slots
+    # entries hold shared-memory byte offsets (layout of csrc/stencil9.cu:
+    # ctab at 0, then 2 coefficient blocks, 2 column blocks, then ubuf)
+    n_slices = n_slices_hint if n_slices_hint is not None else (int(t_arr.max()) + 1 if len(t_arr) else 1)
+    a16 = lambda x: (x + 15) & ~15
+    off = a16(8 * len(coef_tab))
+    off = a16(off + 2 * 8 * n_slices * 10)
+    off = a16(off + 2 * 16 * 4)
+    ubuf_base = off
+    if (ubuf_base + 8 * (n_ubuf + 64)) >= (1 << 18):
+        return None
     n_ent = len(v_arr)
     slots = np.array([slot_of[(int(a), int(b), int(c))] for a, b, c in zip(s_arr, l_arr, t_arr)], dtype=np.int64)
     c_arr = out_off[o_arr] + k_arr if n_ent else np.zeros(0, np.int64)
     ordr = np.lexsort((l_arr, t_arr, c_arr)) if n_ent else np.zeros(0, np.int64)
     counts = np.bincount(c_arr, minlength=n_out_cols) if n_ent else np.zeros(n_out_cols, np.int64)
     starts = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-    packed = (slots[ordr].astype(np.uint64) << np.uint64(14)) | coef_idx[ordr].astype(np.uint64) if n_ent else np.zeros(0, np.uint64)
+    packed = (((ubuf_base + 8 * slots[ordr]).astype(np.uint64) << np.uint64(14))
+              | (8 * coef_idx[ordr]).astype(np.uint64)) if n_ent else np.zeros(0, np.uint64)
     # SELL-32: positions sorted by entry count so a warp's lanes have similar trip counts
     pos_cols = np.argsort(-counts, kind="stable")
     n_chunks = (n_out_cols + 31) // 32
-    pad_word = np.uint64(zero << 14)
+    pad_word = np.uint64((ubuf_base + 8 * zero) << 14)
     chunk_meta = []
     ents = []
     off = 0
@@ -486,6 +499,7 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
         out_col=i32(out_col if n_out_cols else -np.ones(1)),
         out_widths=out_widths,
         stats=stats,
+        n_slices=n_slices,
     )
 
 
@@ -494,6 +508,8 @@ def emulate9(prog: HostProgram9, mats, inputs, inits, alpha, beta):
     is slice t as a SciPy matrix, inputs[s] the (n, width) input arrays."""
     n_rows = mats[0].shape[0]
     ub = np.zeros((n_rows, prog.n_ubuf + 64))
+    a16 = lambda x: (x + 15) & ~15
+    ubase = a16(a16(a16(8 * prog.n_coef) + 2 * 8 * prog.n_slices * 10) + 2 * 16 * 4)
     gi = prog.group_info.reshape(-1, 4)
     base = 0
     for g in range(prog.n_groups):
@@ -515,7 +531,7 @@ def emulate9(prog: HostProgram9, mats, inputs, inits, alpha, beta):
         for e in range(cnt):
             for lane in range(32):
                 w = int(prog.gather_ent[off + e * 32 + lane])
-                acc[:, ch * 32 + lane] += prog.coef_tab[w & 0x3FFF] * ub[:, w >> 14]
+                acc[:, ch * 32 + lane] += prog.coef_tab[(w & 0x3FFF) // 8] * ub[:, ((w >> 14) - ubase) // 8]
     outs = [np.zeros((n_rows, w)) for w in prog.out_widths]
     for pos in range(n_chunks * 32):
         oc = int(prog.out_col[pos])
