@@ -70,7 +70,7 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // 32 consecutive positions (a chunk, one warp) have similar entry counts;
 // chunk j has ccnt[j] entries per lane stored at gent[coff[j] + e*32 + lane];
 // out_col[position] maps back to (output, column) (-1 = padding lane).
-template <int MAXOUT>
+template <int MAXOUT, bool RESIDENT>
 __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
                                                           ViewSet out, ViewSet init, ScalarSet alpha,
                                                           ScalarSet beta) {
@@ -125,9 +125,39 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
     if (tid < 9) cp_async4(cols_s + 16 * buf + tid, pat.colind9 + (int64_t)row * 9 + tid);
   };
 
+  __syncthreads();  // tables and input views visible
+
+  // resident mode: every warp owns at most one group for the whole kernel, so
+  // its 36 V values of the next row can be prefetched during the gather phase
+  constexpr bool resident = RESIDENT;  // host guarantees n_groups <= warps
+  int rbase = 0, rq0 = 0, rq1 = 0;
+  const double* rvb = nullptr;
+  int64_t rld = 0;
+  int rncols = 128;
+  double rv[kCols][9];
+  if (RESIDENT && warp < prog.n_groups) {
+    for (int g = 0; g < warp; ++g) rbase += 128 * (groups[4 * (g + 1) + 3] - groups[4 * g + 3]);
+    const int4 gi = *reinterpret_cast<const int4*>(groups + 4 * warp);
+    rq0 = gi.w;
+    rq1 = groups[4 * (warp + 1) + 3];
+    rvb = in_ptr[gi.x] + gi.y;
+    rld = in_ld[gi.x];
+    rncols = gi.z;
+  }
+  auto load_v = [&](int r, double (&v)[kCols][9]) {
+    const int32_t* cg = pat.colind9 + (int64_t)r * 9;
+#pragma unroll
+    for (int jj = 0; jj < 9; ++jj) {
+      const double* vr = rvb + (int64_t)__ldg(cg + jj) * rld;
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + min(32 * c + lane, rncols - 1));
+    }
+  };
+
   int row = blockIdx.x;
   if (row < pat.n_rows) stage(row, 0);
   cp_async_commit();
+  if (RESIDENT && warp < prog.n_groups && row < pat.n_rows) load_v(row, rv);
   for (int it = 0; row < pat.n_rows; row += gridDim.x, ++it) {
     const int buf = it & 1;
     const int next = row + gridDim.x;
@@ -138,6 +168,26 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
 
     const double* crow = coef_s + buf * ncoef;
     const int32_t* cr = cols_s + 16 * buf;
+    if constexpr (RESIDENT) {
+      // one group per warp for the whole kernel: V of this row was loaded
+      // during the previous row's gather phase
+      if (warp < prog.n_groups) {
+        double2* ub = reinterpret_cast<double2*>(ubuf + rbase + 4 * lane);
+        for (int q = rq0; q < rq1; ++q, ub += 64) {
+          const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[q]);
+          double a[10];
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const double2 p = a2[k];
+            a[2 * k] = p.x;
+            a[2 * k + 1] = p.y;
+          }
+          ub[0] = make_double2(dot9(a, rv[0]), dot9(a, rv[1]));
+          ub[1] = make_double2(dot9(a, rv[2]), dot9(a, rv[3]));
+        }
+        if (next < pat.n_rows) load_v(next, rv);  // prefetch: overlaps barrier + gather
+      }
+    } else {
     int ubase = 0;  // slot base of group g: 128 slots per step, groups in order
     for (int g = 0; g < warp && g < prog.n_groups; ++g)
       ubase += 128 * (groups[4 * (g + 1) + 3] - groups[4 * g + 3]);
@@ -180,6 +230,7 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
       for (int g2 = g; g2 < g + nwarps && g2 < prog.n_groups; ++g2)
         ubase += 128 * (groups[4 * (g2 + 1) + 3] - groups[4 * g2 + 3]);
     }
+    }
     __syncthreads();  // (B) all U of this row in ubuf
 
 #pragma unroll
@@ -188,14 +239,31 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
       if (chunk >= n_chunks) break;
       const int cnt = ccnt[chunk];
       const uint32_t* ge = gent + coff[chunk] + lane;
-      double acc = 0.0;
       // entry = (ubuf byte offset << 14) | ctab byte offset, both relative to
-      // the dynamic shared-memory base
-      for (int e = 0; e < cnt; ++e) {
-        const uint32_t w = ge[32 * e];
-        acc = fma(*reinterpret_cast<const double*>(sm + (w & 0x3FFF)),
-                  *reinterpret_cast<const double*>(sm + (w >> 14)), acc);
+      // the dynamic shared-memory base; 4 entries in flight
+      double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+      int e = 0;
+      for (; e + 3 < cnt; e += 4) {
+        const uint32_t w0 = ge[32 * e], w1 = ge[32 * e + 32], w2 = ge[32 * e + 64], w3 = ge[32 * e + 96];
+        const double c0 = *reinterpret_cast<const double*>(sm + (w0 & 0x3FFF));
+        const double u0 = *reinterpret_cast<const double*>(sm + (w0 >> 14));
+        const double c1 = *reinterpret_cast<const double*>(sm + (w1 & 0x3FFF));
+        const double u1 = *reinterpret_cast<const double*>(sm + (w1 >> 14));
+        const double c2 = *reinterpret_cast<const double*>(sm + (w2 & 0x3FFF));
+        const double u2 = *reinterpret_cast<const double*>(sm + (w2 >> 14));
+        const double c3 = *reinterpret_cast<const double*>(sm + (w3 & 0x3FFF));
+        const double u3 = *reinterpret_cast<const double*>(sm + (w3 >> 14));
+        acc0 = fma(c0, u0, acc0);
+        acc1 = fma(c1, u1, acc1);
+        acc2 = fma(c2, u2, acc2);
+        acc3 = fma(c3, u3, acc3);
       }
+      for (; e < cnt; ++e) {
+        const uint32_t w = ge[32 * e];
+        acc0 = fma(*reinterpret_cast<const double*>(sm + (w & 0x3FFF)),
+                   *reinterpret_cast<const double*>(sm + (w >> 14)), acc0);
+      }
+      const double acc = (acc0 + acc1) + (acc2 + acc3);
       const int oc = ocol[r];
       if (oc >= 0) {
         const int o = oc >> 24, k = oc & 0xFFFFFF;
@@ -210,9 +278,9 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
   cp_async_wait1();
 }
 
-template <int MAXOUT>
-static int launch9(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
-                   const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int threads, cudaStream_t st) {
+template <int MAXOUT, bool RESIDENT>
+static int launch9r(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
+                    const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int threads, cudaStream_t st) {
   const Smem9 L = smem9_layout(pat.n_slices, prog);
   static bool attr_set = false;
   if (!attr_set) {
@@ -220,14 +288,14 @@ static int launch9(const sgk_pattern9& pat, const sgk_program9& prog, const View
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, stencil9_kernel<MAXOUT>);
-    cudaFuncSetAttribute(stencil9_kernel<MAXOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncGetAttributes(&fa, stencil9_kernel<MAXOUT, RESIDENT>);
+    cudaFuncSetAttribute(stencil9_kernel<MAXOUT, RESIDENT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          optin - (int)fa.sharedSizeBytes);
     cudaGetLastError();  // an attribute failure must not poison the launch check
     attr_set = true;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_kernel<MAXOUT>, threads, L.total);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_kernel<MAXOUT, RESIDENT>, threads, L.total);
   if (occ < 1) {
     set_error("stencil9_kernel: program does not fit in shared memory (" + std::to_string(L.total) + " B)");
     return SGK_ELIMIT;
@@ -235,8 +303,16 @@ static int launch9(const sgk_pattern9& pat, const sgk_program9& prog, const View
   int64_t grid = (int64_t)sm_count() * occ;
   if (grid > pat.n_rows) grid = pat.n_rows;
   if (grid < 1) return SGK_OK;
-  stencil9_kernel<MAXOUT><<<(int)grid, threads, L.total, st>>>(pat, prog, in, out, init, a, b);
+  stencil9_kernel<MAXOUT, RESIDENT><<<(int)grid, threads, L.total, st>>>(pat, prog, in, out, init, a, b);
   return check_launch("stencil9_kernel");
+}
+
+template <int MAXOUT>
+static int launch9(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
+                   const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int threads, cudaStream_t st) {
+  if (prog.n_groups <= threads / 32)
+    return launch9r<MAXOUT, true>(pat, prog, in, out, init, a, b, threads, st);
+  return launch9r<MAXOUT, false>(pat, prog, in, out, init, a, b, threads, st);
 }
 
 }  // namespace sgk
