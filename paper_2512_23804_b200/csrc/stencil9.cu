@@ -146,11 +146,21 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
   }
   auto load_v = [&](int r, double (&v)[kCols][9]) {
     const int32_t* cg = pat.colind9 + (int64_t)r * 9;
+    if (rncols == 128) {  // common case: immediate offsets 0/256/512/768 bytes
+      const double* b = rvb + lane;
 #pragma unroll
-    for (int jj = 0; jj < 9; ++jj) {
-      const double* vr = rvb + (int64_t)__ldg(cg + jj) * rld;
+      for (int jj = 0; jj < 9; ++jj) {
+        const double* vr = b + (int64_t)__ldg(cg + jj) * rld;
 #pragma unroll
-      for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + min(32 * c + lane, rncols - 1));
+        for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + 32 * c);
+      }
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 9; ++jj) {
+        const double* vr = rvb + (int64_t)__ldg(cg + jj) * rld;
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + min(32 * c + lane, rncols - 1));
+      }
     }
   };
 
@@ -172,8 +182,8 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
       // one group per warp for the whole kernel: V of this row was loaded
       // during the previous row's gather phase
       if (warp < prog.n_groups) {
-        double2* ub = reinterpret_cast<double2*>(ubuf + rbase + 4 * lane);
-        for (int q = rq0; q < rq1; ++q, ub += 64) {
+        double* ub = ubuf + rbase + lane;
+        for (int q = rq0; q < rq1; ++q, ub += 128) {
           const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[q]);
           double a[10];
 #pragma unroll
@@ -182,8 +192,11 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
             a[2 * k] = p.x;
             a[2 * k + 1] = p.y;
           }
-          ub[0] = make_double2(dot9(a, rv[0]), dot9(a, rv[1]));
-          ub[1] = make_double2(dot9(a, rv[2]), dot9(a, rv[3]));
+          // slot (q, c, lane) = base + 128 q + 32 c + lane: conflict-free STS.64
+          ub[0] = dot9(a, rv[0]);
+          ub[32] = dot9(a, rv[1]);
+          ub[64] = dot9(a, rv[2]);
+          ub[96] = dot9(a, rv[3]);
         }
         if (next < pat.n_rows) load_v(next, rv);  // prefetch: overlaps barrier + gather
       }
@@ -213,8 +226,8 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
           for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + min(32 * c + lane, gi.z - 1));
         }
       }
-      double2* ub = reinterpret_cast<double2*>(ubuf + ubase + 4 * lane);
-      for (int q = gi.w; q < q1; ++q, ub += 64) {
+      double* ub = ubuf + ubase + lane;
+      for (int q = gi.w; q < q1; ++q, ub += 128) {
         const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[q]);
         double a[10];
 #pragma unroll
@@ -223,8 +236,10 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
           a[2 * k] = p.x;
           a[2 * k + 1] = p.y;
         }
-        ub[0] = make_double2(dot9(a, v[0]), dot9(a, v[1]));
-        ub[1] = make_double2(dot9(a, v[2]), dot9(a, v[3]));
+        ub[0] = dot9(a, v[0]);
+        ub[32] = dot9(a, v[1]);
+        ub[64] = dot9(a, v[2]);
+        ub[96] = dot9(a, v[3]);
       }
       // skip the slots of the groups owned by the other warps
       for (int g2 = g; g2 < g + nwarps && g2 < prog.n_groups; ++g2)

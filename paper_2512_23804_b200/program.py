@@ -429,7 +429,7 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
                     key = (int(s), col0 + int(l), int(t))
                     if key not in slot_of:
                         lane, c = int(l) % 32, int(l) // 32
-                        slot_of[key] = n_ubuf + qq * GROUP_COLS + lane * 4 + c
+                        slot_of[key] = n_ubuf + qq * GROUP_COLS + c * 32 + lane
                 executed += GROUP_COLS
             n_ubuf += GROUP_COLS * (len(step_rec) - q0)
             i = j
@@ -464,14 +464,31 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
     out_col = -np.ones(n_chunks * 32, np.int64)
     o_of_c = np.repeat(np.arange(len(out_widths)), out_widths)
     k_of_c = np.concatenate([np.arange(w) for w in out_widths]) if n_out_cols else np.zeros(0, np.int64)
+    zero_words = [np.uint64((ubuf_base + 8 * (zero + z)) << 14) for z in range(32)]
+    bank_of = lambda w: (int(w) >> 17) & 15  # 8-byte bank pair of the ubuf address
     for ch in range(n_chunks):
         cols_ch = pos_cols[32 * ch : 32 * ch + 32]
         cnt = int(counts[cols_ch].max()) if len(cols_ch) else 0
         block = np.full((cnt, 32), pad_word, dtype=np.uint64)
+        lists = []
         for lane, c in enumerate(cols_ch):
-            e = packed[starts[c]:starts[c + 1]]
-            block[: len(e), lane] = e
+            lists.append(list(packed[starts[c]:starts[c + 1]]))
             out_col[32 * ch + lane] = (int(o_of_c[c]) << 24) | int(k_of_c[c])
+        # bank-aware ordering: at every entry row pick, per lane, the entry whose
+        # shared-memory bank pair is least used so far (sums are order-free up
+        # to rounding); lanes that ran out read a zero slot of a free bank pair
+        for e in range(cnt):
+            load = [0] * 16
+            order = sorted(range(len(lists)), key=lambda ln: len(lists[ln]))
+            for ln in order:
+                cand = lists[ln]
+                if cand:
+                    j = min(range(len(cand)), key=lambda i: load[bank_of(cand[i])])
+                    w = cand.pop(j)
+                else:
+                    w = min(zero_words, key=lambda zw: load[bank_of(zw)])
+                load[bank_of(w)] += 1
+                block[e, ln] = w
         chunk_meta.append((cnt, off))
         ents.append(block.reshape(-1))
         off += cnt * 32
@@ -521,7 +538,7 @@ def emulate9(prog: HostProgram9, mats, inputs, inits, alpha, beta):
             for c in range(4):
                 for lane in range(32):
                     col = col0 + min(32 * c + lane, ncols - 1)
-                    ub[:, base + (q - q0) * GROUP_COLS + lane * 4 + c] = mats[t] @ x[:, col]
+                    ub[:, base + (q - q0) * GROUP_COLS + c * 32 + lane] = mats[t] @ x[:, col]
         base += GROUP_COLS * (q1 - q0)
     n_chunks = (prog.n_out_cols + 31) // 32
     meta = prog.gather_ptr.reshape(-1, 2)
