@@ -70,8 +70,11 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // 32 consecutive positions (a chunk, one warp) have similar entry counts;
 // chunk j has ccnt[j] entries per lane stored at gent[coff[j] + e*32 + lane];
 // out_col[position] maps back to (output, column) (-1 = padding lane).
+#ifndef SGK_S9_MINB
+#define SGK_S9_MINB 2
+#endif
 template <int MAXOUT, bool RESIDENT>
-__global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
+__global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
                                                           ViewSet out, ViewSet init, ScalarSet alpha,
                                                           ScalarSet beta) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -129,7 +132,6 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
 
   // resident mode: every warp owns at most one group for the whole kernel, so
   // its 36 V values of the next row can be prefetched during the gather phase
-  constexpr bool resident = RESIDENT;  // host guarantees n_groups <= warps
   int rbase = 0, rq0 = 0, rq1 = 0;
   const double* rvb = nullptr;
   int64_t rld = 0;
@@ -183,15 +185,33 @@ __global__ void __launch_bounds__(256, 2) stencil9_kernel(sgk_pattern9 pat, sgk_
       // during the previous row's gather phase
       if (warp < prog.n_groups) {
         double* ub = ubuf + rbase + lane;
+#if SGK_S9_PIPE
+        double an[10];
+        if (rq0 < rq1) {
+          const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[rq0]);
+#pragma unroll
+          for (int k = 0; k < 5; ++k) { const double2 p = a2[k]; an[2 * k] = p.x; an[2 * k + 1] = p.y; }
+        }
+#endif
         for (int q = rq0; q < rq1; ++q, ub += 128) {
-          const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[q]);
           double a[10];
+#if SGK_S9_PIPE
+#pragma unroll
+          for (int k = 0; k < 10; ++k) a[k] = an[k];
+          {
+            const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[q + 1 < rq1 ? q + 1 : q]);
+#pragma unroll
+            for (int k = 0; k < 5; ++k) { const double2 p = a2[k]; an[2 * k] = p.x; an[2 * k + 1] = p.y; }
+          }
+#else
+          const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[q]);
 #pragma unroll
           for (int k = 0; k < 5; ++k) {
             const double2 p = a2[k];
             a[2 * k] = p.x;
             a[2 * k + 1] = p.y;
           }
+#endif
           // slot (q, c, lane) = base + 128 q + 32 c + lane: conflict-free STS.64
           ub[0] = dot9(a, rv[0]);
           ub[32] = dot9(a, rv[1]);
