@@ -249,8 +249,11 @@ def run_program(
     beta: list[float] | None = None,
     threads: int = 256,
     stream: torch.cuda.Stream | None = None,
+    rows: tuple[int, int] | None = None,
 ) -> None:
-    """Launch program_kernel: outputs[o][:, col0+k] = alpha*gather + beta*init."""
+    """Launch program_kernel: outputs[o][:, col0+k] = alpha*gather + beta*init.
+    `rows=(a, b)` restricts the launch to mesh rows [a, b) (9-point fast path
+    only; used by the pipelined host-buffer path)."""
     n_out = len(outputs)
     if n_out != len(program.out_widths):
         raise ValueError("output count does not match the program")
@@ -269,6 +272,18 @@ def run_program(
     lib = _lib.lib()
     p9 = pattern.pattern9() if FAST9 else None
     f9 = program.fast9(pattern.n_slices) if p9 is not None else None
+    if rows is not None:
+        if f9 is None:
+            raise ValueError("row-range launches need the 9-point fast path")
+        r0, r1 = rows
+        if not 0 <= r0 <= r1 <= pattern.n_rows:
+            raise ValueError("row range out of bounds")
+        p9 = _lib.Pattern9(n_rows=r1 - r0, n_slices=p9.n_slices, colind9=p9.colind9 + 4 * 9 * r0,
+                           coef10=p9.coef10 + 8 * 10 * p9.n_slices * r0)
+        for arr in (out_arr, init_arr):
+            for v in arr:
+                if v.ptr:
+                    v.ptr = v.ptr + 8 * v.ld * r0
     if f9 is not None:
         h9 = f9.host
         chunks = (h9.n_out_cols + 31) // 32
