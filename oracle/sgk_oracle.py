@@ -32,6 +32,10 @@ __all__ = [
     "splu_ref",
     "steady_kkt_apply",
     "steady_precond_apply",
+    "time_kkt_apply",
+    "time_lead",
+    "time_precond_apply",
+    "time_weights",
 ]
 
 
@@ -395,3 +399,77 @@ def kron_apply_rows(couplings, operators, x, rows):
     for h, a in zip(couplings, operators):
         out += _xh(a[r0:r1] @ x, h)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Time-dependent all-at-once KKT and the parallel-in-time preconditioner
+# (reference operators.py:204-324, preconditioners.py:198-208, 278-333).
+# Packed layout as in the reference: [y steps; u steps; lambda steps], each
+# step an F-order (column-major) vec of an (N, n_xi) block.
+
+def _split_time(v, n_t, n_h, n_xi):
+    size = n_h * n_xi
+    v = np.asarray(v, dtype=np.float64)
+    return [np.stack([v[(b * n_t + k) * size:(b * n_t + k + 1) * size].reshape((n_h, n_xi), order="F")
+                      for k in range(n_t)]) for b in range(3)]
+
+
+def _join_time(y, u, lam):
+    return np.concatenate([blk[k].reshape(-1, order="F") for blk in (y, u, lam) for k in range(blk.shape[0])])
+
+
+def time_weights(n_t):
+    """Trapezoid weights (1/2, 1, ..., 1, 1/2) and tau = 1/n_t (operators.py:212-223)."""
+    w = np.ones(n_t)
+    w[0] = 0.5
+    w[-1] = 0.5
+    return 1.0 / n_t, w
+
+
+def time_kkt_apply(mass, stiffness, couplings, weight_diag, beta, n_t, v):
+    """time_kkt_apply, operators.py:284-309."""
+    n_h, n_xi = mass.shape[0], len(weight_diag)
+    tau, w = time_weights(n_t)
+    y, u, lam = _split_time(v, n_t, n_h, n_xi)
+    cp = couplings[: len(stiffness)]
+    step = lambda x: mass @ x + tau * kron_apply(cp, stiffness, x)
+    ry, ru, rl = np.empty_like(y), np.empty_like(u), np.empty_like(lam)
+    wd = weight_diag[None, :]
+    for k in range(n_t):
+        at_lam = step(lam[k])
+        if k + 1 < n_t:
+            at_lam -= mass @ lam[k + 1]
+        ry[k] = tau * w[k] * ((mass @ y[k]) * wd) - at_lam
+        ru[k] = beta * tau * w[k] * (mass @ u[k]) + tau * (mass @ lam[k])
+        a_y = step(y[k])
+        if k > 0:
+            a_y -= mass @ y[k - 1]
+        rl[k] = -a_y + tau * (mass @ u[k])
+    return _join_time(ry, ru, rl)
+
+
+def time_lead(mass, stiffness, beta, gamma, n_t):
+    """time_lead_terms, preconditioners.py:198-208."""
+    tau = 1.0 / n_t
+    shift = 1.0 + tau * np.sqrt((1.0 + gamma) / beta)
+    return [(shift * mass + tau * stiffness[0]).tocsr()] + [(tau * a).tocsr() for a in stiffness[1:]]
+
+
+def time_precond_apply(mass, stiffness, couplings, weight_diag, beta, gamma, boundaries, n_tau, lead_lu, n_t, r,
+                       mass_its=5, richardson_steps=1):
+    """TimeKKTPreconditioner.apply, preconditioners.py:294-312 (Chebyshev mass solves)."""
+    n_h, n_xi = mass.shape[0], len(weight_diag)
+    tau, w = time_weights(n_t)
+    terms = time_lead(mass, stiffness, beta, gamma, n_t)
+    cp = couplings[: len(stiffness)]
+    ry, ru, rl = _split_time(r, n_t, n_h, n_xi)
+    wc = weight_diag[None, :]
+    vy, vu, vl = np.empty_like(ry), np.empty_like(ru), np.empty_like(rl)
+    for k in range(n_t):
+        dk = w[k]
+        vy[k] = chebyshev_mass_solve(mass, ry[k], mass_its) / (tau * dk * wc)
+        vu[k] = chebyshev_mass_solve(mass, ru[k], mass_its) / (beta * tau * dk)
+        z1 = richardson_hgs(cp, terms, boundaries, n_tau, lead_lu, rl[k], richardson_steps)
+        ww = dk * (mass @ z1) * wc
+        vl[k] = tau * richardson_hgs(cp, terms, boundaries, n_tau, lead_lu, ww, richardson_steps)
+    return _join_time(vy, vu, vl)

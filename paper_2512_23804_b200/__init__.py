@@ -25,6 +25,7 @@ _SUBMODULES = (
     "linalg",
     "preconditioners",
     "krylov",
+    "timedep",
     "vec",
     "device",
 )

@@ -167,10 +167,44 @@ def gen_basis_fem():
     np.savez_compressed(OUT / "basis_fem.npz", **out)
 
 
+def gen_time(name, n, m_xi, p, n_t, beta):
+    """Time-dependent all-at-once KKT (operators.py:204-324) and the PINT
+    preconditioner (preconditioners.py:198-208, 278-333)."""
+    basis, bench, fem, krylov, ops, pre, problems, rf = _ref()
+    rng = np.random.default_rng(SEED + 100 + n)
+    bundle = problems.build_time_problem(n=n, m_xi=m_xi, p=p, sigma_k=0.3, beta=beta, n_t=n_t,
+                                         coefficient="affine")
+    sys_ = bundle.system
+    st = sys_.steady
+    out = {"n": np.array(n), "beta": np.array(beta), "gamma": np.array(st.gamma), "n_t": np.array(n_t),
+           "boundaries": np.array(bundle.partition.boundaries, dtype=np.int64), "n_terms": np.array(st.n_terms)}
+    csr_parts("M", st.mass, out)
+    for t, a in enumerate(st.stiffness):
+        csr_parts(f"A{t}", a, out)
+    for t, h in enumerate(st.triple.matrices):
+        csr_parts(f"H{t}", h, out)
+    out["weight_diag"] = st.triple.weight_diagonal
+    out["target"] = st.target
+    out["y0"] = sys_.initial_state
+    size = 3 * sys_.block_size()
+    v = rng.standard_normal(size)
+    out["v"] = v
+    out["kkt"] = ops.time_kkt_apply(sys_, v)
+    out["rhs"] = ops.time_rhs(sys_)
+    for n_tau in sorted({1, st.n_terms}):
+        prec = pre.build_time_preconditioner(sys_, bundle.partition, mass_solver="cheb5", n_tau=n_tau)
+        out[f"pint_tau{n_tau}"] = prec.apply(v)
+    xs, rep = bench.solve_bundle(bundle, "cheb5", st.n_terms, 1e-6)
+    out["fgmres_x"] = xs
+    out["fgmres_iters"] = np.array(rep.iterations)
+    np.savez_compressed(OUT / f"{name}.npz", **out)
+
+
 if __name__ == "__main__":
     gen_kron_random()
     gen_basis_fem()
     gen_steady("steady_affine_n6", 6, 2, 2, "affine", None, 0.3, 1e-2)
     gen_steady("steady_logn_n4", 4, 2, 2, "lognormal", 4, 0.3, 1e-2)
+    gen_time("time_affine_n6", 6, 2, 2, 4, 1e-2)
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
