@@ -326,6 +326,55 @@ def solve_block(cfg_id, betas, with_cpu=False):
     return out
 
 
+def time_solve_block(with_cpu: bool):
+    """all-at-once time-dependent KKT with the PINT
+    preconditioner inside the reference FGMRES (tol 1e-6, Chebyshev-5, hGS
+    Richardson-1, n_tau = n_A) on the paper's (3,3) lognormal setting:
+    n=32 (N=961), m=3, p=3 (n_xi=20), coefficient degree 6 (84 terms), N_t=8."""
+    import torch
+
+    from paper_2512_23804_b200.krylov import FgmresConfig, fgmres
+    from paper_2512_23804_b200.problems import ConfigSpec, build_problem, steady_system
+    from paper_2512_23804_b200.timedep import (TimeKKT, build_time_preconditioner, build_time_stencil,
+                                               time_kkt_apply, time_rhs, to_device_layout)
+
+    spec = ConfigSpec("time_paper", "control", 32, 3, 3, "hermite", "lognormal", 0.2, 1.0,
+                      coefficient_degree=6, beta=1e-4, lo=-1.0, hi=1.0)
+    b = build_problem(spec, kl_method="dense")
+    st = steady_system(b)
+    sys_ = TimeKKT(steady=st, stencil=build_time_stencil(8), initial_state=np.zeros((st.n_h, st.n_xi)))
+    t0 = time.perf_counter()
+    prec = build_time_preconditioner(sys_, b.partition, "cheb5")
+    rhs = time_rhs(sys_)
+    bd = to_device_layout(sys_, rhs)
+    prec.apply(bd)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    times = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x, rep = fgmres(lambda v: time_kkt_apply(sys_, v), lambda v: prec.apply(v), bd, FgmresConfig(tol=1e-6))
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    out = {"dofs": 3 * sys_.block_size(), "n_t": 8, "n_xi": st.n_xi, "n_terms": st.n_terms,
+           "gpu": {"iterations": rep.iterations, "converged": bool(rep.converged), "seconds": times[1],
+                   "first_solve_seconds": times[0], "setup_seconds": t_setup}}
+    if with_cpu:
+        import oracle
+
+        m, a = st.mass, st.stiffness
+        cp = st.triple.matrices[: st.n_terms]
+        lead = oracle.splu_ref(oracle.time_lead(m, a, st.beta, st.gamma, 8)[0])
+        op = lambda v: oracle.time_kkt_apply(m, a, cp, st.triple.weight_diagonal, st.beta, 8, v)
+        pr = lambda v: oracle.time_precond_apply(m, a, cp, st.triple.weight_diagonal, st.beta, st.gamma,
+                                                 b.partition.boundaries, st.n_terms, lead, 8, v)
+        t0 = time.perf_counter()
+        _, its, conv, _ = oracle.fgmres(op, pr, rhs, 1e-6)
+        out["cpu_port"] = {"iterations": its, "converged": bool(conv), "seconds": time.perf_counter() - t0, "cores": 1}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -456,6 +505,8 @@ def run_ours(args):
         solves = {"cfg2": solve_block(2, [1e-2])}
         if args.solve_cfg5:
             solves["cfg5"] = solve_block(5, [1e-2, 1e-4, 1e-6])
+        if args.solve_time:
+            solves["time_dependent"] = time_solve_block(args.time_cpu)
         line["solves"] = solves
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -472,6 +523,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--solve-cfg5", action="store_true")
+    ap.add_argument("--solve-time", action="store_true", help="time-dependent PINT solve (SURVEY 8(f) row 1)")
+    ap.add_argument("--time-cpu", action="store_true", help="also time the CPU port of the time-dependent solve")
     ap.add_argument("--ref-budget", type=float, default=3.0)
     args = ap.parse_args()
     if args.warmup < 3:
