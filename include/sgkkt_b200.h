@@ -177,10 +177,12 @@ typedef struct {
   const double* vals;
   const int32_t* group_ptr;   /* [n_groups+1] row ranges                   */
   const int32_t* group_order; /* [n_groups] topological (level) order      */
+  const int32_t* gdep_ptr;    /* [n_groups+1] distinct dependency groups   */
+  const int32_t* gdep;        /* of each group (CSR)                       */
   const int32_t* work_row;    /* [n]                                       */
   const int32_t* io_row;      /* [n]                                       */
   const double* diag_inv;     /* [n] or NULL                               */
-  int32_t* flags;             /* [n * ceil(width/CW)] scratch              */
+  int32_t* flags;             /* [n_groups * chunks] scratch               */
   int32_t* ticket;            /* [1] scratch                               */
 } sgk_trigroups;
 
@@ -203,8 +205,9 @@ int sgk_trisolve(const sgk_trifactor* L, const sgk_trifactor* U,
                  const sgk_segview* b, const sgk_segview* x, double* work,
                  int32_t width, int32_t epoch, void* stream);
 
-/* Same result as sgk_trisolve, grouped task granularity (flags per
- * (row, sgk_trisolve_grouped_chunk_cols()-column chunk)).                   */
+/* Same result as sgk_trisolve, grouped task granularity (one readiness flag
+ * per (group, chunk) with chunks of 1..16 columns; `work` must hold
+ * n x (width rounded up to a multiple of 16) doubles).                       */
 int32_t sgk_trisolve_grouped_chunk_cols(void);
 int sgk_trisolve_grouped(const sgk_trigroups* L, const sgk_trigroups* U,
                          const sgk_segview* b, const sgk_segview* x,

@@ -169,9 +169,24 @@ static int launch_chunked(const sgk_trifactor& L, const sgk_trifactor& U, const 
 constexpr int GMAX = 32;
 constexpr int GCW_MIN = 1;  // narrowest grouped chunk (sizes the flag array)
 
+template <int GCW>
+__device__ __forceinline__ void load_cols(const double* __restrict__ p, double (&x)[GCW]) {
+  // p is GCW-aligned inside a row padded to a multiple of GCW columns
+  if constexpr (GCW == 1) {
+    x[0] = __ldcg(p);
+  } else {
+#pragma unroll
+    for (int c = 0; c < GCW; c += 2) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(p + c));
+      x[c] = v.x;
+      x[c + 1] = v.y;
+    }
+  }
+}
+
 template <bool FWD, int GCW, int GEPL>
 __global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview io, double* __restrict__ work,
-                                                  int width, int n_chunks, int epoch) {
+                                                  int width, int ldw, int n_chunks, int epoch) {
   __shared__ double part[GMAX][GCW];
   __shared__ double ys[GMAX][GCW];
   __shared__ double lg[GMAX][GMAX + 1];  // dense in-group block (strictly lower)
@@ -192,32 +207,19 @@ __global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview i
     const int c0 = chunk * GCW;
     const int w = min(GCW, width - c0);
 
-    // 0: wait for every outside dependency of the whole group at once (the
-    //    group's rows are contiguous in CSR; all polls of a thread in flight)
+    // 0: wait for the groups this group depends on (host-computed distinct
+    //    dependency groups; one flag per (group, chunk))
     {
-      const int ea = __ldg(t.rowptr + r0), eb = __ldg(t.rowptr + r1);
-      for (int base = ea; base < eb; base += 4 * blockDim.x) {
-        int cj[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = base + tid + u * blockDim.x;
-          const int c = e < eb ? __ldg(t.colind + e) : -1;
-          cj[u] = c < r0 ? c : -1;
-        }
-        for (;;) {
-          bool ready = true;
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (cj[u] >= 0) ready &= ld_relaxed(t.flags + (int64_t)cj[u] * n_chunks + chunk) == epoch;
-          if (ready) break;
-          __nanosleep(64);
-        }
+      const int da = __ldg(t.gdep_ptr + gi), db = __ldg(t.gdep_ptr + gi + 1);
+      for (int d = da + tid; d < db; d += blockDim.x) {
+        const int32_t* fl = t.flags + (int64_t)__ldg(t.gdep + d) * n_chunks + chunk;
+        while (ld_relaxed(fl) != epoch) __nanosleep(64);
       }
       fence_acq_rel();
     }
     __syncthreads();
 
-    // 1: outside contributions, rows over warps (all dependencies ready)
+    // 1: outside contributions, rows over warps, lanes over entries
     for (int r = warp; r < g; r += nwarps) {
       const int p = r0 + r;
       const int e0 = __ldg(t.rowptr + p), e2 = __ldg(t.rowptr + p + 1);
@@ -234,17 +236,17 @@ __global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview i
 #pragma unroll
         for (int u = 0; u < GEPL; ++u) {
           const int e = base + lane + 32 * u;
-          const int c = e < e1 ? __ldg(t.colind + e) : -1;
-          cj[u] = c;
-          vj[u] = c >= 0 ? __ldg(t.vals + e) : 0.0;
+          // past the end: re-read the last outside entry (a finished
+          // dependency, so its value is final and finite) with weight 0
+          const int ec = min(e, e1 - 1);
+          cj[u] = __ldg(t.colind + ec);
+          vj[u] = e < e1 ? __ldg(t.vals + ec) : 0.0;
         }
         double xv[GEPL][GCW];
 #pragma unroll
         for (int u = 0; u < GEPL; ++u) {
-          const int wr = t.reversed ? t.n - 1 - max(cj[u], 0) : max(cj[u], 0);
-          const double* zr = work + (int64_t)wr * width + c0;
-#pragma unroll
-          for (int c = 0; c < GCW; ++c) xv[u][c] = (cj[u] >= 0 && c < w) ? __ldcg(zr + c) : 0.0;
+          const int wr = t.reversed ? t.n - 1 - cj[u] : cj[u];
+          load_cols<GCW>(work + (int64_t)wr * ldw + c0, xv[u]);
         }
 #pragma unroll
         for (int u = 0; u < GEPL; ++u)
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview i
         for (int c = 1; c < GCW; ++c)
           if (lane == c) s = acc[c];
         const double init = FWD ? seg_load(io, __ldg(t.io_row + p), c0 + lane)
-                                : __ldcg(work + (int64_t)__ldg(t.work_row + p) * width + c0 + lane);
+                                : __ldcg(work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + lane);
         part[r][lane] = init + s;
       }
     }
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview i
       double pr[GCW];
       const bool mine = lane < g;
 #pragma unroll
-      for (int c = 0; c < GCW; ++c) pr[c] = mine ? part[lane][c] : 0.0;
+      for (int c = 0; c < GCW; ++c) pr[c] = (mine && c < w) ? part[lane][c] : 0.0;
       const double d = (!FWD && mine) ? __ldg(t.diag_inv + r0 + lane) : 1.0;
       for (int j = 0; j < g; ++j) {
         const double l = (lane > j && mine) ? lg[lane][j] : 0.0;
@@ -289,18 +291,17 @@ __global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview i
     }
     __syncthreads();
 
-    // 3: write back, fence, publish
+    // 3: write back (padded columns too: keeps the loads above unconditional),
+    //    fence, publish the group flag for this chunk
     for (int i = tid; i < g * GCW; i += blockDim.x) {
       const int r = i / GCW, c = i - r * GCW;
-      if (c < w) {
-        const int p = r0 + r;
-        __stcg(work + (int64_t)__ldg(t.work_row + p) * width + c0 + c, ys[r][c]);
-        if (!FWD) seg_store(io, __ldg(t.io_row + p), c0 + c, ys[r][c]);
-      }
+      const int p = r0 + r;
+      __stcg(work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + c, c < w ? ys[r][c] : 0.0);
+      if (!FWD && c < w) seg_store(io, __ldg(t.io_row + p), c0 + c, ys[r][c]);
     }
     fence_acq_rel();
     __syncthreads();
-    if (tid < g) st_relaxed(t.flags + (int64_t)(r0 + tid) * n_chunks + chunk, epoch);
+    if (tid == 0) st_relaxed(t.flags + (int64_t)gi * n_chunks + chunk, epoch);
   }
 }
 
@@ -309,6 +310,7 @@ static int launch_grouped_t(const sgk_trigroups& L, const sgk_trigroups& U, cons
                             const sgk_segview& x, double* work, int width, int epoch, int threads, int occ_cap,
                             cudaStream_t st) {
   const int n_chunks = (width + GCW - 1) / GCW;
+  const int ldw = n_chunks * GCW;  // work rows padded to whole chunks
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_group<true, GCW, GEPL>, threads, 0);
   if (occ < 1) occ = 1;
@@ -319,10 +321,10 @@ static int launch_grouped_t(const sgk_trigroups& L, const sgk_trigroups& U, cons
   if (grid < 1) grid = 1;
   cudaMemsetAsync(L.ticket, 0, sizeof(int32_t), st);
   cudaMemsetAsync(U.ticket, 0, sizeof(int32_t), st);
-  trsv_group<true, GCW, GEPL><<<(int)grid, threads, 0, st>>>(L, b, work, width, n_chunks, epoch);
+  trsv_group<true, GCW, GEPL><<<(int)grid, threads, 0, st>>>(L, b, work, width, ldw, n_chunks, epoch);
   int rc = check_launch("trsv_group<fwd>");
   if (rc) return rc;
-  trsv_group<false, GCW, GEPL><<<(int)grid, threads, 0, st>>>(U, x, work, width, n_chunks, epoch);
+  trsv_group<false, GCW, GEPL><<<(int)grid, threads, 0, st>>>(U, x, work, width, ldw, n_chunks, epoch);
   return check_launch("trsv_group<bwd>");
 }
 
@@ -335,10 +337,11 @@ static int launch_grouped(const sgk_trigroups& L, const sgk_trigroups& U, const 
                           const sgk_segview& x, double* work, int width, int epoch, cudaStream_t st) {
   // chunk width by RHS width (env overrides for tuning experiments)
   // measured on B200 (tools/tri_sweep.py, profiles/r01_trisolve_sweep.txt):
-  // narrow chunks win up to ~40 columns, 4-column chunks above; 16 warps per task
+  // narrow chunks win up to ~40 columns, 4-column chunks above; 16 warps per
+  // task, 8 for very wide blocks (more tasks in flight: cfg5 w330 31 -> 26 ms)
   int cw = env_int("SGKKT_TRI_CW", width <= 8 ? 1 : (width <= 40 ? 2 : 4));
-  const int threads = env_int("SGKKT_TRI_THREADS", 512);
-  const int occ_cap = env_int("SGKKT_TRI_OCC", 2);
+  const int threads = env_int("SGKKT_TRI_THREADS", width > 200 ? 256 : 512);
+  const int occ_cap = env_int("SGKKT_TRI_OCC", width > 200 ? 4 : 2);
   const int epl = env_int("SGKKT_TRI_EPL", 8);
   if (cw <= 1) return launch_grouped_t<1, 16>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
   if (cw <= 2) return launch_grouped_t<2, 16>(L, U, b, x, work, width, epoch, threads, occ_cap, st);

@@ -82,6 +82,23 @@ GROUP_MAX = 32
 GROUPED = __import__("os").environ.get("SGKKT_TRISOLVE", "grouped") != "rows"
 
 
+def group_dependencies(strict: csr_matrix, gptr: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Distinct groups each group depends on (its outside columns), as CSR."""
+    n = strict.shape[0]
+    ng = len(gptr) - 1
+    if n == 0 or strict.nnz == 0:
+        return np.zeros(ng + 1, dtype=np.int64), np.zeros(0, np.int64)
+    gid = np.repeat(np.arange(ng), np.diff(gptr))
+    rg = gid[np.repeat(np.arange(n), np.diff(strict.indptr))]
+    cg = gid[strict.indices]
+    outside = cg != rg
+    key = np.unique(rg[outside].astype(np.int64) * ng + cg[outside])
+    src, dep = key // ng, key % ng
+    ptr = np.zeros(ng + 1, dtype=np.int64)
+    np.add.at(ptr, src + 1, 1)
+    return np.cumsum(ptr), dep
+
+
 def chain_groups(strict: csr_matrix, max_rows: int = GROUP_MAX) -> tuple[np.ndarray, np.ndarray, int]:
     """Group consecutive rows of a strictly lower triangle into chains (row k
     joins the group of row k-1 when it depends on row k-1), and order the
@@ -137,10 +154,13 @@ def _grouped(strict: csr_matrix, work_row, io_row, dinv):
         _f64(dinv) if dinv is not None else None, torch.zeros(1, dtype=torch.int32, device=dev),
         _i32(split if n else [0]),
     ]
+    dptr, deps = group_dependencies(strict, gptr)
+    bufs += [_i32(dptr), _i32(deps if len(deps) else [0])]
     st = _lib.TriGroups(
         n=strict.shape[0], n_groups=len(gptr) - 1, reversed=int(n > 0 and work_row[0] != 0), pad=0, rowptr=bufs[0].data_ptr(), split=bufs[9].data_ptr(),
         colind=bufs[1].data_ptr(),
         vals=bufs[2].data_ptr(), group_ptr=bufs[3].data_ptr(), group_order=bufs[4].data_ptr(),
+        gdep_ptr=bufs[10].data_ptr(), gdep=bufs[11].data_ptr(),
         work_row=bufs[5].data_ptr(), io_row=bufs[6].data_ptr(),
         diag_inv=bufs[7].data_ptr() if bufs[7] is not None else None, flags=None, ticket=bufs[8].data_ptr(),
     )
@@ -250,7 +270,8 @@ class TriangularFactors:
 
         bv = segview(b_segs)
         xv = segview(x_segs)
-        work = torch.empty((self.n, width), dtype=torch.float64, device=b_segs[0][0].device)
+        work = torch.empty((self.n, -(-width // 16) * 16 if GROUPED else width), dtype=torch.float64,
+                           device=b_segs[0][0].device)
         self._ensure_flags(width)
         self.epoch += 1
         if GROUPED:
