@@ -106,17 +106,19 @@ typedef struct {
 
 /* Contiguous-group uniform schedule: group g covers input columns
  * [col0, col0+ncols) (ncols <= 128) of input s; lane L of the owning warp
- * holds columns col0 + 32c + L (c < 4).  Step q evaluates term t_q for the
- * column slots c whose slot base sb_c >= 0 (32 U slots each).
- * group_info[g] = {s, col0, ncols, q0};  step_rec[q] = {t, sb0, sb1, sb2,
- * sb3, 0, 0, 0} (inactive slots point at the 32 trash slots n_ubuf..);
- * gather in SELL-32 form: gather_ptr[2j], gather_ptr[2j+1] = entry count and
- * offset of chunk j (32 output positions), entries at off + e*32 + lane,
- * packed (ubuf byte offset << 14) | coef_tab byte offset, both relative to
- * the kernel's dynamic shared memory (layout: coef_tab, 2 coefficient
- * blocks, 2 column blocks, ubuf — so the program is compiled for the
- * pattern's n_slices); padding reads the zero slots n_ubuf+32..;
- * out_col[position] = (output<<24)|column or -1.                            */
+ * holds columns col0 + 32c + L (c < 4).  group_info[g] = {s, col0, ncols, q0}
+ * (steps q0 .. group_info[g+1].q0).  Step q evaluates term t_q for the four
+ * column slots: step_rec[q] = t_q | (sw_q << 16), sw_q < 16, and the product
+ * of lane L, slot c lands in ubuf slot gbase + 128(q-q0) + 32c + (L ^ sw_q)
+ * (gbase = slots of the groups before; 32 trash and 32 zero slots follow the
+ * n_ubuf product slots).  Gather, SELL-32 (32 output positions per chunk,
+ * a chunk never spans two outputs): gather_ptr[2j], [2j+1] = row count and
+ * offset of chunk j; entries at off + e*32 + lane, packed (ubuf byte
+ * offset << 14) | coef_tab byte offset, both relative to the kernel's dynamic
+ * shared memory (layout: coef_tab, 2 coefficient blocks, 2 column blocks,
+ * ubuf — so the program is compiled for the pattern's n_slices); padding
+ * reads the zero slots.  Chunk j is gathered by warp j % (CTA warps); out_col[position]
+ * = (output<<24)|column or -1.                                              */
 typedef struct {
   int32_t n_groups;
   int32_t n_steps;
@@ -125,13 +127,13 @@ typedef struct {
   int32_t n_coef;
   int32_t n_gather;
   int32_t n_slices;          /* pattern slices the entry offsets assume      */
-  int32_t pad;
+  int32_t n_chunks;          /* >= ceil(n_out_cols/32)                      */
   const int32_t* group_info; /* [(n_groups+1)*4]                            */
-  const int32_t* step_rec;   /* [n_steps*8]                                 */
+  const int32_t* step_rec;   /* [n_steps]                                   */
   const double* coef_tab;    /* [n_coef]                                    */
-  const int32_t* gather_ptr; /* [2*ceil(n_out_cols/32)]                     */
+  const int32_t* gather_ptr; /* [2*n_chunks]                                */
   const uint32_t* gather_ent;/* [n_gather]                                  */
-  const int32_t* out_col;    /* [32*ceil(n_out_cols/32)]                    */
+  const int32_t* out_col;    /* [32*n_chunks]                               */
 } sgk_program9;
 
 /* Same contract as sgk_program_apply for a padded 9-point pattern.  Returns

@@ -73,7 +73,7 @@ class Pattern9(ctypes.Structure):
 class Program9(ctypes.Structure):
     _fields_ = [
         ("n_groups", c_i32), ("n_steps", c_i32), ("n_ubuf", c_i32), ("n_out_cols", c_i32),
-        ("n_coef", c_i32), ("n_gather", c_i32), ("n_slices", c_i32), ("pad", c_i32), ("group_info", c_vp),
+        ("n_coef", c_i32), ("n_gather", c_i32), ("n_slices", c_i32), ("n_chunks", c_i32), ("group_info", c_vp),
         ("step_rec", c_vp),
         ("coef_tab", c_vp), ("gather_ptr", c_vp), ("gather_ent", c_vp), ("out_col", c_vp),
     ]

@@ -21,6 +21,9 @@
 namespace sgk {
 
 constexpr int kCols = 4;  // column slots per lane
+#ifndef SGK_VLD
+#define SGK_VLD __ldg
+#endif
 
 // Shared-memory map.  ubuf holds n_ubuf U slots + 32 trash slots (inactive
 // (step, column-slot) pairs store there) + 32 zero slots (gather padding).
@@ -39,7 +42,7 @@ __host__ __device__ inline Smem9 smem9_layout(int n_slices, const sgk_program9& 
   s.ubuf = off;   off = align16(off + sizeof(double) * ((size_t)p.n_ubuf + 64));
   s.steps = off;  off = align16(off + sizeof(int32_t) * (size_t)p.n_steps);
   s.groups = off; off = align16(off + sizeof(int32_t) * 4 * (size_t)(p.n_groups + 1));
-  const size_t n_chunks = ((size_t)p.n_out_cols + 31) / 32;
+  const size_t n_chunks = (size_t)p.n_chunks;
   s.ccnt = off;   off = align16(off + sizeof(int32_t) * n_chunks);
   s.coff = off;   off = align16(off + sizeof(int32_t) * n_chunks);
   s.gent = off;   off = align16(off + sizeof(uint32_t) * (size_t)p.n_gather);
@@ -73,7 +76,10 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 #ifndef SGK_S9_MINB
 #define SGK_S9_MINB 2
 #endif
-template <int MAXOUT, bool RESIDENT>
+#ifndef SGK_S9_IL
+#define SGK_S9_IL 1  // gather chunks walked together (1 measured best: 1.47 vs 1.73 ms at 4)
+#endif
+template <int MAXOUT, bool RESIDENT, bool ONEOUT>
 __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
                                                           ViewSet out, ViewSet init, ScalarSet alpha,
                                                           ScalarSet beta) {
@@ -93,7 +99,7 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
-  const int n_chunks = (prog.n_out_cols + 31) >> 5;
+  const int n_chunks = prog.n_chunks;
   __shared__ const double* in_ptr[SGK_MAX_IO];
   __shared__ int64_t in_ld[SGK_MAX_IO];
   if (tid < SGK_MAX_IO) {
@@ -112,6 +118,7 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
     coff[i] = prog.gather_ptr[2 * i + 1];
   }
   for (int i = tid; i < prog.n_gather; i += blockDim.x) gent[i] = prog.gather_ent[i];
+
   for (int i = tid; i < 64; i += blockDim.x) ubuf[prog.n_ubuf + i] = 0.0;
 
   int ocol[MAXOUT];
@@ -154,14 +161,14 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
       for (int jj = 0; jj < 9; ++jj) {
         const double* vr = b + (int64_t)__ldg(cg + jj) * rld;
 #pragma unroll
-        for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + 32 * c);
+        for (int c = 0; c < kCols; ++c) v[c][jj] = SGK_VLD(vr + 32 * c);
       }
     } else {
 #pragma unroll
       for (int jj = 0; jj < 9; ++jj) {
         const double* vr = rvb + (int64_t)__ldg(cg + jj) * rld;
 #pragma unroll
-        for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + min(32 * c + lane, rncols - 1));
+        for (int c = 0; c < kCols; ++c) v[c][jj] = SGK_VLD(vr + min(32 * c + lane, rncols - 1));
       }
     }
   };
@@ -206,35 +213,38 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
       // one group per warp for the whole kernel: V of this row was loaded
       // during the previous row's gather phase
       if (warp < prog.n_groups) {
-        double* ub = ubuf + rbase + lane;
-#if SGK_S9_PIPE
-        double an[10];
+        double* ubq = ubuf + rbase;
+        // software pipeline: the step record and the first 4 coefficients of
+        // step q+1 are loaded during step q, so each step's first 16 DFMAs
+        // start without waiting on shared memory
+        int recn = rq0 < rq1 ? steps[rq0] : 0;
+        double2 p01 = make_double2(0.0, 0.0), p23 = p01;
         if (rq0 < rq1) {
-          const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[rq0]);
-#pragma unroll
-          for (int k = 0; k < 5; ++k) { const double2 p = a2[k]; an[2 * k] = p.x; an[2 * k + 1] = p.y; }
+          const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (recn & 0xFFFF));
+          p01 = a2[0];
+          p23 = a2[1];
         }
-#endif
-        for (int q = rq0; q < rq1; ++q, ub += 128) {
+        for (int q = rq0; q < rq1; ++q, ubq += 128) {
+          const int rec = recn;
+          double* ub = ubq + (lane ^ (rec >> 16));  // swizzled slot, conflict-free STS
           double a[10];
-#if SGK_S9_PIPE
-#pragma unroll
-          for (int k = 0; k < 10; ++k) a[k] = an[k];
+          a[0] = p01.x; a[1] = p01.y; a[2] = p23.x; a[3] = p23.y;
           {
-            const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[q + 1 < rq1 ? q + 1 : q]);
+            const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (rec & 0xFFFF));
 #pragma unroll
-            for (int k = 0; k < 5; ++k) { const double2 p = a2[k]; an[2 * k] = p.x; an[2 * k + 1] = p.y; }
+            for (int k = 2; k < 5; ++k) {
+              const double2 p = a2[k];
+              a[2 * k] = p.x;
+              a[2 * k + 1] = p.y;
+            }
           }
-#else
-          const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[q]);
-#pragma unroll
-          for (int k = 0; k < 5; ++k) {
-            const double2 p = a2[k];
-            a[2 * k] = p.x;
-            a[2 * k + 1] = p.y;
+          recn = steps[q + 1 < rq1 ? q + 1 : q];
+          {
+            const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (recn & 0xFFFF));
+            p01 = a2[0];
+            p23 = a2[1];
           }
-#endif
-          // slot (q, c, lane) = base + 128 q + 32 c + lane: conflict-free STS.64
+          // slot (q, c, lane) = base + 128 q + 32 c + (lane ^ sw_q)
           ub[0] = dot9(a, rv[0]);
           ub[32] = dot9(a, rv[1]);
           ub[64] = dot9(a, rv[2]);
@@ -280,19 +290,21 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
         for (int jj = 0; jj < 9; ++jj) {
           const double* vr = base + cr[jj] * vld;
 #pragma unroll
-          for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + 32 * c);
+          for (int c = 0; c < kCols; ++c) v[c][jj] = SGK_VLD(vr + 32 * c);
         }
       } else {
 #pragma unroll
         for (int jj = 0; jj < 9; ++jj) {
           const double* vr = vbase + cr[jj] * vld;
 #pragma unroll
-          for (int c = 0; c < kCols; ++c) v[c][jj] = __ldg(vr + min(32 * c + lane, gi.z - 1));
+          for (int c = 0; c < kCols; ++c) v[c][jj] = SGK_VLD(vr + min(32 * c + lane, gi.z - 1));
         }
       }
-      double* ub = ubuf + ubase + lane;
-      for (int q = gi.w; q < q1; ++q, ub += 128) {
-        const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * steps[q]);
+      double* ubq = ubuf + ubase;
+      for (int q = gi.w; q < q1; ++q, ubq += 128) {
+        const int rec = steps[q];
+        double* ub = ubq + (lane ^ (rec >> 16));
+        const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (rec & 0xFFFF));
         double a[10];
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
@@ -310,54 +322,64 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
         ubase += 128 * (groups[4 * (g2 + 1) + 3] - groups[4 * g2 + 3]);
     }
     }
+
     __syncthreads();  // (B) all U of this row in ubuf
 
+    // gather: the warp's chunks (chunk = warp + r*nwarps) are walked
+    // together, IL at a time, so their entry rows are independent loads in
+    // flight; entry = (ubuf byte offset << 14) | ctab byte offset relative to
+    // the dynamic shared memory; the host orders every lane's entries so the
+    // rows' U loads repeat few bank pairs per half-warp
+    constexpr int IL = MAXOUT < SGK_S9_IL ? MAXOUT : SGK_S9_IL;
 #pragma unroll
-    for (int r = 0; r < MAXOUT; ++r) {
-      const int chunk = warp + r * nwarps;
-      if (chunk >= n_chunks) break;
-      const int cnt = ccnt[chunk];
-      const uint32_t* ge = gent + coff[chunk] + lane;
-      // entry = (ubuf byte offset << 14) | ctab byte offset, both relative to
-      // the dynamic shared-memory base; 4 entries in flight
-      double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-      int e = 0;
-      for (; e + 3 < cnt; e += 4) {
-        const uint32_t w0 = ge[32 * e], w1 = ge[32 * e + 32], w2 = ge[32 * e + 64], w3 = ge[32 * e + 96];
-        const double c0 = *reinterpret_cast<const double*>(sm + (w0 & 0x3FFF));
-        const double u0 = *reinterpret_cast<const double*>(sm + (w0 >> 14));
-        const double c1 = *reinterpret_cast<const double*>(sm + (w1 & 0x3FFF));
-        const double u1 = *reinterpret_cast<const double*>(sm + (w1 >> 14));
-        const double c2 = *reinterpret_cast<const double*>(sm + (w2 & 0x3FFF));
-        const double u2 = *reinterpret_cast<const double*>(sm + (w2 >> 14));
-        const double c3 = *reinterpret_cast<const double*>(sm + (w3 & 0x3FFF));
-        const double u3 = *reinterpret_cast<const double*>(sm + (w3 >> 14));
-        acc0 = fma(c0, u0, acc0);
-        acc1 = fma(c1, u1, acc1);
-        acc2 = fma(c2, u2, acc2);
-        acc3 = fma(c3, u3, acc3);
+    for (int rb = 0; rb < MAXOUT; rb += IL) {
+      int cnt[IL], gofs[IL];
+      double acc0[IL], acc1[IL];
+      int emax = 0;
+#pragma unroll
+      for (int i = 0; i < IL; ++i) {
+        const int chunk = warp + (rb + i) * nwarps;
+        const bool ok = chunk < n_chunks;
+        cnt[i] = ok ? ccnt[chunk] : 0;
+        gofs[i] = (ok ? coff[chunk] : 0) + lane;
+        acc0[i] = 0.0;
+        acc1[i] = 0.0;
+        emax = max(emax, cnt[i]);
       }
-      for (; e < cnt; ++e) {
-        const uint32_t w = ge[32 * e];
-        acc0 = fma(*reinterpret_cast<const double*>(sm + (w & 0x3FFF)),
-                   *reinterpret_cast<const double*>(sm + (w >> 14)), acc0);
+      for (int e = 0; e < emax; e += 2) {
+#pragma unroll
+        for (int i = 0; i < IL; ++i) {
+          if (e < cnt[i]) {
+            const uint32_t w0 = gent[gofs[i] + 32 * e];
+            acc0[i] = fma(*reinterpret_cast<const double*>(sm + (w0 & 0x3FFF)),
+                          *reinterpret_cast<const double*>(sm + (w0 >> 14)), acc0[i]);
+          }
+          if (e + 1 < cnt[i]) {
+            const uint32_t w1 = gent[gofs[i] + 32 * e + 32];
+            acc1[i] = fma(*reinterpret_cast<const double*>(sm + (w1 & 0x3FFF)),
+                          *reinterpret_cast<const double*>(sm + (w1 >> 14)), acc1[i]);
+          }
+        }
       }
-      const double acc = (acc0 + acc1) + (acc2 + acc3);
-      const int oc = ocol[r];
-      if (oc >= 0) {
-        const int o = oc >> 24, k = oc & 0xFFFFFF;
-        double y = pick_s(alpha, o) * acc;
-        const sgk_view& iv = pick(init, o);
-        if (iv.ptr != nullptr) y += pick_s(beta, o) * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
-        const sgk_view& ov = pick(out, o);
-        ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
+#pragma unroll
+      for (int i = 0; i < IL; ++i) {
+        const int oc = ocol[rb + i];
+        if (oc >= 0) {
+          const double acc = acc0[i] + acc1[i];
+          const int o = ONEOUT ? 0 : oc >> 24, k = oc & 0xFFFFFF;
+          double y = pick_s(alpha, o) * acc;
+          const sgk_view& iv = pick(init, o);
+          if (iv.ptr != nullptr) y += pick_s(beta, o) * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
+          const sgk_view& ov = pick(out, o);
+          ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
+        }
       }
     }
   }
   cp_async_wait1();
 }
 
-template <int MAXOUT, bool RESIDENT>
+template <int MAXOUT, bool RESIDENT, bool ONEOUT>
 static int launch9r(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
                     const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int threads, cudaStream_t st) {
   const Smem9 L = smem9_layout(pat.n_slices, prog);
@@ -367,14 +389,14 @@ static int launch9r(const sgk_pattern9& pat, const sgk_program9& prog, const Vie
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, stencil9_kernel<MAXOUT, RESIDENT>);
-    cudaFuncSetAttribute(stencil9_kernel<MAXOUT, RESIDENT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncGetAttributes(&fa, stencil9_kernel<MAXOUT, RESIDENT, ONEOUT>);
+    cudaFuncSetAttribute(stencil9_kernel<MAXOUT, RESIDENT, ONEOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          optin - (int)fa.sharedSizeBytes);
     cudaGetLastError();  // an attribute failure must not poison the launch check
     attr_set = true;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_kernel<MAXOUT, RESIDENT>, threads, L.total);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_kernel<MAXOUT, RESIDENT, ONEOUT>, threads, L.total);
   if (occ < 1) {
     set_error("stencil9_kernel: program does not fit in shared memory (" + std::to_string(L.total) + " B)");
     return SGK_ELIMIT;
@@ -382,16 +404,20 @@ static int launch9r(const sgk_pattern9& pat, const sgk_program9& prog, const Vie
   int64_t grid = (int64_t)sm_count() * occ;
   if (grid > pat.n_rows) grid = pat.n_rows;
   if (grid < 1) return SGK_OK;
-  stencil9_kernel<MAXOUT, RESIDENT><<<(int)grid, threads, L.total, st>>>(pat, prog, in, out, init, a, b);
+  stencil9_kernel<MAXOUT, RESIDENT, ONEOUT><<<(int)grid, threads, L.total, st>>>(pat, prog, in, out, init, a, b);
   return check_launch("stencil9_kernel");
 }
 
 template <int MAXOUT>
 static int launch9(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
-                   const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int threads, cudaStream_t st) {
-  if (prog.n_groups <= threads / 32)
-    return launch9r<MAXOUT, true>(pat, prog, in, out, init, a, b, threads, st);
-  return launch9r<MAXOUT, false>(pat, prog, in, out, init, a, b, threads, st);
+                   const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int n_out, int threads,
+                   cudaStream_t st) {
+  const bool res = prog.n_groups <= threads / 32;
+  if (n_out == 1)
+    return res ? launch9r<MAXOUT, true, true>(pat, prog, in, out, init, a, b, threads, st)
+               : launch9r<MAXOUT, false, true>(pat, prog, in, out, init, a, b, threads, st);
+  return res ? launch9r<MAXOUT, true, false>(pat, prog, in, out, init, a, b, threads, st)
+             : launch9r<MAXOUT, false, false>(pat, prog, in, out, init, a, b, threads, st);
 }
 
 }  // namespace sgk
@@ -425,13 +451,14 @@ extern "C" int sgk_stencil9_apply(const sgk_pattern9* pat, const sgk_program9* p
     b.s[i] = beta[i];
   }
   if (pat->n_rows == 0 || prog->n_out_cols == 0) return SGK_OK;
-  const int per = ((prog->n_out_cols + 31) / 32 + threads / 32 - 1) / (threads / 32);
+  SGK_REQUIRE(prog->n_chunks * 32 >= prog->n_out_cols, "sgk_stencil9_apply: n_chunks too small");
+  const int per = (prog->n_chunks + threads / 32 - 1) / (threads / 32);
   cudaStream_t st = (cudaStream_t)stream;
-  if (per <= 1) return launch9<1>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
-  if (per <= 2) return launch9<2>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
-  if (per <= 4) return launch9<4>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
-  if (per <= 8) return launch9<8>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
-  if (per <= 16) return launch9<16>(*pat, *prog, vin, vout, vinit, a, b, threads, st);
+  if (per <= 1) return launch9<1>(*pat, *prog, vin, vout, vinit, a, b, n_out, threads, st);
+  if (per <= 2) return launch9<2>(*pat, *prog, vin, vout, vinit, a, b, n_out, threads, st);
+  if (per <= 4) return launch9<4>(*pat, *prog, vin, vout, vinit, a, b, n_out, threads, st);
+  if (per <= 8) return launch9<8>(*pat, *prog, vin, vout, vinit, a, b, n_out, threads, st);
+  if (per <= 16) return launch9<16>(*pat, *prog, vin, vout, vinit, a, b, n_out, threads, st);
   set_error("sgk_stencil9_apply: too many output columns for one CTA");
   return SGK_ELIMIT;
 }

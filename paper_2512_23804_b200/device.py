@@ -185,7 +185,8 @@ class _Program9:
         b = self._bufs
         self.struct = _lib.Program9(
             n_groups=host.n_groups, n_steps=host.n_steps, n_ubuf=host.n_ubuf, n_out_cols=host.n_out_cols,
-            n_coef=host.n_coef, n_gather=host.n_gather, n_slices=host.n_slices, pad=0,
+            n_coef=host.n_coef, n_gather=host.n_gather, n_slices=host.n_slices,
+            n_chunks=len(host.out_col) // 32 if host.n_out_cols else 0,
             group_info=b[0].data_ptr(), step_rec=b[1].data_ptr(),
             coef_tab=b[2].data_ptr(), gather_ptr=b[3].data_ptr(), gather_ent=b[4].data_ptr(),
             out_col=b[5].data_ptr(),
@@ -286,8 +287,7 @@ def run_program(
                     v.ptr = v.ptr + 8 * v.ld * r0
     if f9 is not None:
         h9 = f9.host
-        chunks = (h9.n_out_cols + 31) // 32
-        warps = min(8, max(1, h9.n_groups, -(-chunks // 16)))
+        warps = h9.warps
         rc = lib.sgk_stencil9_apply(ctypes.byref(p9), ctypes.byref(f9.struct), len(inputs), in_arr,
                                     n_out, out_arr, init_arr, a, b, 32 * warps, _lib.stream_ptr(stream))
         if rc != -3:  # -3: does not fit in shared memory -> general kernel

@@ -32,6 +32,7 @@ Compilation:
 from __future__ import annotations
 
 from dataclasses import dataclass, field
+import os
 
 import numpy as np
 
@@ -369,15 +370,206 @@ class HostProgram9:
     out_widths: tuple[int, ...]
     stats: dict = field(default_factory=dict)
     n_slices: int = 0
+    warps: int = 1  # CTA warps the gather layout assumes (chunk c -> warp c % warps)
 
 
 GROUP_COLS = 128  # 4 column slots x 32 lanes
 
 
+def stencil9_warps(n_groups: int, n_chunks: int) -> int:
+    """Warps per CTA for stencil9_kernel: one per column group (resident V
+    registers) and at most 16 gather chunks per warp, 8 at most."""
+    return min(8, max(1, n_groups, -(-n_chunks // 16)))
+# bank-layout local search budget per program (deterministic; off by default:
+# cfg4 matvec 1.725 ms with it vs 1.728 ms without, and it costs ~3 s/program)
+SEARCH_MOVES = int(os.environ.get("SGKKT_S9_SEARCH_MOVES", "0"))
+
+
+def _ubuf_base(n_coef: int, n_slices: int) -> int:
+    """Byte offset of ubuf in stencil9_kernel's dynamic shared memory."""
+    a16 = lambda x: (x + 15) & ~15
+    return a16(a16(a16(8 * n_coef) + 2 * 8 * n_slices * 10) + 2 * 16 * 4)
+
+
+def _class_layout(counts, out_off, n_cls):
+    """Output positions: each output's columns sorted by their per-class entry
+    counts (so a 32-lane chunk has similar counts per class), padded to whole
+    chunks (a chunk never spans two outputs).  Returns (col_at_pos, pos_of_col)."""
+    col_at_pos = []
+    for o in range(len(out_off) - 1):
+        cols = np.arange(out_off[o], out_off[o + 1])
+        if len(cols):
+            keys = tuple(-counts[cols, c] for c in range(n_cls))
+            cols = cols[np.lexsort(keys)]
+        pad = (-len(cols)) % 32
+        col_at_pos.extend(cols.tolist() + [-1] * pad)
+    col_at_pos = np.array(col_at_pos, dtype=np.int64)
+    pos_of_col = np.full(int(out_off[-1]), -1, np.int64)
+    valid = col_at_pos >= 0
+    pos_of_col[col_at_pos[valid]] = np.nonzero(valid)[0]
+    return col_at_pos, pos_of_col
+
+
+class _BankSearch:
+    """Deterministic local search over (per-step slot swizzle, output position
+    permutation) minimising the modelled U-gather shared-memory wavefronts
+    sum_cells max(rows(cell), max bank-pair load(cell)), cell = (chunk, class,
+    half-warp): a 64-bit LDS is served per half-warp, so 16 distinct 8-byte
+    bank pairs per half-warp is conflict-free."""
+
+    def __init__(self, e_col, e_cls, e_q, e_lane, counts, col_at_pos, pos_of_col, n_steps, n_cls, ubase_dbl,
+                 out_of_col):
+        self.e_col, self.e_cls, self.e_q, self.e_lane = e_col, e_cls, e_q, e_lane
+        self.col_at_pos, self.pos_of_col = col_at_pos.copy(), pos_of_col.copy()
+        self.n_cls, self.ubase = n_cls, ubase_dbl
+        self.sw = (5 * np.arange(n_steps)) & 15
+        n_pos = len(col_at_pos)
+        self.n_cells = (n_pos // 32) * n_cls * 2
+        cp = counts[np.maximum(col_at_pos, 0)] * (col_at_pos >= 0)[:, None]
+        self.R = np.repeat(cp.reshape(-1, 32, n_cls).max(1).reshape(-1), 2)  # rows per cell
+        self.by_q = [np.nonzero(e_q == q)[0] for q in range(n_steps)]
+        self.by_col = {}
+        for i, cc in enumerate(e_col.tolist()):
+            self.by_col.setdefault(cc, []).append(i)
+        key = {}
+        for cc in range(len(pos_of_col)):
+            key.setdefault((int(out_of_col[cc]), counts[cc].tobytes()), []).append(cc)
+        self.twins = [v for v in key.values() if len(v) > 1]
+        self.H = np.zeros((self.n_cells, 16), np.int64)
+        self._apply(np.arange(len(e_col)), 1)
+
+    def cells(self, idx):
+        pos = self.pos_of_col[self.e_col[idx]]
+        return ((pos >> 5) * self.n_cls + self.e_cls[idx]) * 2 + ((pos >> 4) & 1)
+
+    def banks(self, idx):
+        return (self.ubase + (self.e_lane[idx] ^ self.sw[self.e_q[idx]])) & 15
+
+    def cost_cells(self, cells):
+        # U wavefronts of a half-warp over the chunk's rows >= max(rows, max
+        # bank-pair load); _assign_rows gets close to it
+        cells = np.unique(cells)
+        return int(np.maximum(self.R[cells], self.H[cells].max(1)).sum())
+
+    def total(self):
+        return self.cost_cells(np.arange(self.n_cells))
+
+    def _apply(self, idx, sign):
+        np.add.at(self.H, (self.cells(idx), self.banks(idx)), sign)
+
+    def _swap(self, p1, p2):
+        c1, c2 = int(self.col_at_pos[p1]), int(self.col_at_pos[p2])
+        self.col_at_pos[p1], self.col_at_pos[p2] = c2, c1
+        if c1 >= 0:
+            self.pos_of_col[c1] = p2
+        if c2 >= 0:
+            self.pos_of_col[c2] = p1
+
+    def run(self, moves, seed=12345):
+        rng = np.random.default_rng(seed)
+        n_steps = len(self.sw)
+        for _ in range(moves):
+            if rng.random() < 0.5 and n_steps:
+                q = int(rng.integers(n_steps))
+                idx = self.by_q[q]
+                if not len(idx):
+                    continue
+                cells = np.unique(self.cells(idx))
+                before = self.cost_cells(cells)
+                old = self.sw[q]
+                self._apply(idx, -1)
+                self.sw[q] = int(rng.integers(16))
+                self._apply(idx, 1)
+                if self.cost_cells(cells) > before:
+                    self._apply(idx, -1)
+                    self.sw[q] = old
+                    self._apply(idx, 1)
+                continue
+            # swap two positions inside one chunk, or two columns of one output
+            # with identical per-class counts (rows per cell stay unchanged)
+            if rng.random() < 0.5 or not self.twins:
+                p1 = int(rng.integers(len(self.col_at_pos)))
+                p2 = (p1 & ~31) + int(rng.integers(32))
+            else:
+                tw = self.twins[int(rng.integers(len(self.twins)))]
+                i1, i2 = rng.choice(len(tw), 2, replace=False)
+                p1, p2 = int(self.pos_of_col[tw[int(i1)]]), int(self.pos_of_col[tw[int(i2)]])
+            c1, c2 = int(self.col_at_pos[p1]), int(self.col_at_pos[p2])
+            if p1 == p2 or (c1 < 0 and c2 < 0):
+                continue
+            idx = np.array(self.by_col.get(c1, []) + self.by_col.get(c2, []), dtype=np.int64)
+            if not len(idx):
+                self._swap(p1, p2)
+                continue
+            cells0 = self.cells(idx)
+            self._swap(p1, p2)
+            cells = np.unique(np.concatenate([cells0, self.cells(idx)]))
+            self._swap(p1, p2)
+            before = self.cost_cells(cells)
+            self._apply(idx, -1)
+            self._swap(p1, p2)
+            self._apply(idx, 1)
+            if self.cost_cells(cells) > before:
+                self._apply(idx, -1)
+                self._swap(p1, p2)
+                self._apply(idx, 1)
+
+
+def _assign_rows(lists, zero_of_bank):
+    """Order each lane's gather entries over the chunk's rows (rows = the
+    longest lane list) so that each row's 64-bit U loads hit as few repeated
+    bank pairs per half-warp as possible: per row and half-warp a maximum
+    bipartite matching lanes -> bank pairs (lanes that must take an entry this
+    row first), the rest on the least-loaded bank pair.  lists[lane] =
+    [(payload, bank)]; returns (rows, 32) payloads, idle lanes reading a zero
+    slot on a free bank pair (zero_of_bank[bank] = payload)."""
+    n_rows = max((len(x) for x in lists), default=0)
+    out = np.zeros((n_rows, 32), np.int64)
+    rem = [list(x) for x in lists]
+    for r in range(n_rows):
+        left = n_rows - r
+        for half in (0, 16):
+            lanes = range(half, half + 16)
+            must = [ln for ln in lanes if len(rem[ln]) >= left]
+            opt = sorted((ln for ln in lanes if 0 < len(rem[ln]) < left), key=lambda ln: -len(rem[ln]))
+            owner, choice = {}, {}
+
+            def augment(ln, seen):
+                for item in rem[ln]:
+                    bk = item[1]
+                    if bk in seen:
+                        continue
+                    seen.add(bk)
+                    if bk not in owner or augment(owner[bk], seen):
+                        owner[bk] = ln
+                        choice[ln] = item
+                        return True
+                return False
+
+            for ln in must + opt:
+                augment(ln, set())
+            load = [0] * 16
+            for ln, item in choice.items():
+                load[item[1]] += 1
+            for ln in must:
+                if ln not in choice:  # forced conflict: least-loaded bank pair
+                    item = min(rem[ln], key=lambda it: load[it[1]])
+                    choice[ln] = item
+                    load[item[1]] += 1
+            free = iter(b for b in range(16) if load[b] == 0)
+            for ln in lanes:
+                if ln in choice:
+                    rem[ln].remove(choice[ln])
+                    out[r, ln] = choice[ln][0]
+                else:
+                    out[r, ln] = zero_of_bank[next(free, ln & 15)]
+    return out
+
+
 def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | None = None,
-                     n_slices_hint: int | None = None) -> HostProgram9 | None:
+                     n_slices_hint: int | None = None, search: bool = True) -> HostProgram9 | None:
     """Schedule for stencil9_kernel, or None when the gather does not fit its
-    packed encoding (> 16384 distinct coefficients)."""
+    encodings (> 2048 distinct coefficients) or shared memory."""
     out_widths = tuple(int(w) for w in out_widths)
     couplings = [c for c in couplings if c is not None and len(c.rows)]
     out_off = np.concatenate([[0], np.cumsum(out_widths)]).astype(np.int64)
@@ -393,16 +585,20 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
         s_arr = t_arr = l_arr = o_arr = k_arr = np.zeros(0, np.int64)
         v_arr = np.zeros(0)
     coef_tab, coef_idx = np.unique(v_arr, return_inverse=True)
+    coef_idx = np.asarray(coef_idx, np.int64).reshape(-1)
     if len(coef_tab) == 0:
         coef_tab = np.zeros(1)
     if len(coef_tab) * 8 > (1 << 14):
         return None
     # groups of 128 consecutive columns per input (the last one shifted left so
     # it stays 128 wide when the input spans >= 128 columns: a column covered
-    # twice is computed twice, its product slot is taken from the first group)
+    # twice is computed twice, its product slot is taken from the first group).
+    # Product (s, l, t) lives at slot base + (lane0 ^ sw[q]), base = group base
+    # + 128 qq + 32 c: a per-step XOR swizzle (< 16) keeps the producer's STS
+    # conflict-free and spreads the gather over bank pairs.
     group_info = []
     step_rec = []
-    slot_of = {}  # (s, l, t) -> slot
+    prod_of = {}  # (s, l, t) -> (q, base, lane0)
     n_ubuf = 0
     executed = 0
     for s in np.unique(s_arr):
@@ -427,79 +623,97 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
                 step_rec.append(int(t))
                 for l in np.unique(gl[gt == t]):
                     key = (int(s), col0 + int(l), int(t))
-                    if key not in slot_of:
-                        lane, c = int(l) % 32, int(l) // 32
-                        slot_of[key] = n_ubuf + qq * GROUP_COLS + c * 32 + lane
+                    if key not in prod_of:
+                        prod_of[key] = (q0 + qq, n_ubuf + qq * GROUP_COLS + (int(l) // 32) * 32, int(l) % 32)
                 executed += GROUP_COLS
             n_ubuf += GROUP_COLS * (len(step_rec) - q0)
             i = j
     n_steps = len(step_rec)
+    if n_steps and max(step_rec) >= (1 << 16):
+        return None
     group_info.append((0, 0, 0, n_steps))
     zero = n_ubuf + 32  # 32 zero slots after 32 spare slots
-    # entries hold shared-memory byte offsets (layout of csrc/stencil9.cu:
-    # ctab at 0, then 2 coefficient blocks, 2 column blocks, then ubuf)
     n_slices = n_slices_hint if n_slices_hint is not None else (int(t_arr.max()) + 1 if len(t_arr) else 1)
-    a16 = lambda x: (x + 15) & ~15
-    off = a16(8 * len(coef_tab))
-    off = a16(off + 2 * 8 * n_slices * 10)
-    off = a16(off + 2 * 16 * 4)
-    ubuf_base = off
+    ubuf_base = _ubuf_base(len(coef_tab), n_slices)
     if (ubuf_base + 8 * (n_ubuf + 64)) >= (1 << 18):
         return None
+    ubase_dbl = ubuf_base // 8
     n_ent = len(v_arr)
-    slots = np.array([slot_of[(int(a), int(b), int(c))] for a, b, c in zip(s_arr, l_arr, t_arr)], dtype=np.int64)
+    prod = np.array([prod_of[(int(a), int(b), int(c))] for a, b, c in zip(s_arr, l_arr, t_arr)],
+                    dtype=np.int64).reshape(-1, 3)
+    e_q, e_base, e_lane = prod[:, 0], prod[:, 1], prod[:, 2]
     c_arr = out_off[o_arr] + k_arr if n_ent else np.zeros(0, np.int64)
-    ordr = np.lexsort((l_arr, t_arr, c_arr)) if n_ent else np.zeros(0, np.int64)
-    counts = np.bincount(c_arr, minlength=n_out_cols) if n_ent else np.zeros(n_out_cols, np.int64)
-    starts = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-    packed = (((ubuf_base + 8 * slots[ordr]).astype(np.uint64) << np.uint64(14))
-              | (8 * coef_idx[ordr]).astype(np.uint64)) if n_ent else np.zeros(0, np.uint64)
-    # SELL-32: positions sorted by entry count so a warp's lanes have similar trip counts
-    pos_cols = np.argsort(-counts, kind="stable")
-    n_chunks = (n_out_cols + 31) // 32
-    pad_word = np.uint64((ubuf_base + 8 * zero) << 14)
-    chunk_meta = []
-    ents = []
-    off = 0
-    out_col = -np.ones(n_chunks * 32, np.int64)
     o_of_c = np.repeat(np.arange(len(out_widths)), out_widths)
     k_of_c = np.concatenate([np.arange(w) for w in out_widths]) if n_out_cols else np.zeros(0, np.int64)
-    zero_words = [np.uint64((ubuf_base + 8 * (zero + z)) << 14) for z in range(32)]
-    bank_of = lambda w: (int(w) >> 17) & 15  # 8-byte bank pair of the ubuf address
+    stats_extra = {}
+    sw = (5 * np.arange(n_steps)) & 15
+    counts = np.zeros((n_out_cols, 1), np.int64)
+    if n_ent:
+        np.add.at(counts, (c_arr, 0), 1)
+    col_at_pos, pos_of_col = _class_layout(counts, out_off, 1)
+    zeros_e = np.zeros(n_ent, np.int64)
+    if n_ent:
+        bs = _BankSearch(c_arr, zeros_e, e_q, e_lane, counts, col_at_pos, pos_of_col, n_steps, 1, ubase_dbl, o_of_c)
+        stats_extra["bank_model_start"] = bs.total()
+        if search and SEARCH_MOVES:
+            bs.run(min(SEARCH_MOVES, 8 * n_ent))
+        stats_extra["bank_model"] = bs.total()
+        sw, col_at_pos, pos_of_col = bs.sw, bs.col_at_pos, bs.pos_of_col
+    n_chunks = len(col_at_pos) // 32
+    slot = e_base + (e_lane ^ sw[e_q]) if n_ent else np.zeros(0, np.int64)
+    bank = (ubase_dbl + slot) & 15
+    payload = ((ubuf_base + 8 * slot) << 14) | (8 * coef_idx)
+    zero_of_bank = {(ubase_dbl + zero + z) & 15: (ubuf_base + 8 * (zero + z)) << 14 for z in range(16)}
+    per = {}
+    pos_e = pos_of_col[c_arr] if n_ent else np.zeros(0, np.int64)
+    for i in range(n_ent):
+        pos = int(pos_e[i])
+        per.setdefault(pos >> 5, {}).setdefault(pos & 31, []).append((int(payload[i]), int(bank[i])))
+    blocks = []
     for ch in range(n_chunks):
-        cols_ch = pos_cols[32 * ch : 32 * ch + 32]
-        cnt = int(counts[cols_ch].max()) if len(cols_ch) else 0
-        block = np.full((cnt, 32), pad_word, dtype=np.uint64)
-        lists = []
-        for lane, c in enumerate(cols_ch):
-            lists.append(list(packed[starts[c]:starts[c + 1]]))
-            out_col[32 * ch + lane] = (int(o_of_c[c]) << 24) | int(k_of_c[c])
-        # bank-aware ordering: at every entry row pick, per lane, the entry whose
-        # shared-memory bank pair is least used so far (sums are order-free up
-        # to rounding); lanes that ran out read a zero slot of a free bank pair
-        for e in range(cnt):
-            load = [0] * 16
-            order = sorted(range(len(lists)), key=lambda ln: len(lists[ln]))
-            for ln in order:
-                cand = lists[ln]
-                if cand:
-                    j = min(range(len(cand)), key=lambda i: load[bank_of(cand[i])])
-                    w = cand.pop(j)
-                else:
-                    w = min(zero_words, key=lambda zw: load[bank_of(zw)])
-                load[bank_of(w)] += 1
-                block[e, ln] = w
-        chunk_meta.append((cnt, off))
-        ents.append(block.reshape(-1))
-        off += cnt * 32
+        lanes = per.get(ch)
+        rows = _assign_rows([lanes.get(ln, []) for ln in range(32)], zero_of_bank) if lanes else \
+            np.zeros((0, 32), np.int64)
+        blocks.append(rows.astype(np.uint32))
+    # chunk c is gathered by warp c % warps (the launcher's warp count): give
+    # each warp chunks of similar row counts
+    n_groups = len(group_info) - 1
+    warps = stencil9_warps(n_groups, n_chunks)
+    per_warp = -(-n_chunks // warps) if n_chunks else 0
+    n_slots = per_warp * warps
+    order = sorted(range(n_chunks), key=lambda c: -len(blocks[c]))
+    slot_of_chunk = {}
+    for j, c in enumerate(order):
+        w, r = j // per_warp, j % per_warp
+        slot_of_chunk[c] = w + r * warps
+    chunk_meta = [(0, 0)] * n_slots
+    out_col = -np.ones(n_slots * 32, np.int64)
+    ents, off = [], 0
+    inv = {v: c for c, v in slot_of_chunk.items()}
+    for j in range(n_slots):
+        c = inv.get(j)
+        if c is None:
+            chunk_meta[j] = (0, off)
+            continue
+        blk = blocks[c]
+        chunk_meta[j] = (len(blk), off)
+        ents.append(blk.reshape(-1))
+        off += blk.size
+        cols = col_at_pos[32 * c: 32 * c + 32]
+        safe = np.maximum(cols, 0)
+        out_col[32 * j: 32 * j + 32] = np.where(cols >= 0, (o_of_c[safe] << 24) | k_of_c[safe], -1)
+    stats_extra["gather_rows"] = int(sum(len(b) for b in blocks))
+    stats_extra["warps"] = warps
     gather_ptr = np.array(chunk_meta, dtype=np.int64).reshape(-1) if chunk_meta else np.zeros(2, np.int64)
-    ent = np.concatenate(ents) if ents else np.zeros(0, np.uint64)
+    ent = np.concatenate(ents).astype(np.uint32) if ents else np.zeros(0, np.uint32)
     n_gather = int(len(ent))
-    useful = len(slot_of)
-    stats = {"mode": "stencil9", "n_products": int(useful), "n_groups": len(group_info) - 1,
-             "n_steps": n_steps, "lane_efficiency": float(useful / executed) if executed else 1.0,
-             "n_gather": int(n_ent), "n_gather_padded": n_gather, "n_ubuf": int(n_ubuf),
-             "n_coef": int(len(coef_tab))}
+    useful = len(prod_of)
+    step_words = (np.array(step_rec, dtype=np.int64) | (np.asarray(sw, np.int64) << 16)) if n_steps else np.zeros(1)
+    stats = {"mode": "stencil9", "n_products": int(useful),
+             "n_groups": len(group_info) - 1, "n_steps": n_steps,
+             "lane_efficiency": float(useful / executed) if executed else 1.0,
+             "n_gather": int(n_ent), "n_gather_words": n_gather, "n_ubuf": int(n_ubuf),
+             "n_coef": int(len(coef_tab)), **stats_extra}
     i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
     return HostProgram9(
         n_groups=len(group_info) - 1,
@@ -509,14 +723,15 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
         n_coef=int(len(coef_tab)),
         n_gather=n_gather,
         group_info=i32(np.array(group_info, dtype=np.int64).reshape(-1)),
-        step_rec=i32(np.array(step_rec, dtype=np.int64) if step_rec else np.zeros(1)),
+        step_rec=i32(step_words),
         coef_tab=np.ascontiguousarray(coef_tab if len(coef_tab) else np.zeros(1)),
         gather_ptr=i32(gather_ptr),
-        gather_ent=np.ascontiguousarray(ent.astype(np.uint32) if n_gather else np.zeros(1, np.uint32)),
-        out_col=i32(out_col if n_out_cols else -np.ones(1)),
+        gather_ent=np.ascontiguousarray(ent if n_gather else np.zeros(1, np.uint32)),
+        out_col=i32(out_col if len(out_col) else -np.ones(1)),
         out_widths=out_widths,
         stats=stats,
         n_slices=n_slices,
+        warps=warps,
     )
 
 
@@ -525,8 +740,7 @@ def emulate9(prog: HostProgram9, mats, inputs, inits, alpha, beta):
     is slice t as a SciPy matrix, inputs[s] the (n, width) input arrays."""
     n_rows = mats[0].shape[0]
     ub = np.zeros((n_rows, prog.n_ubuf + 64))
-    a16 = lambda x: (x + 15) & ~15
-    ubase = a16(a16(a16(8 * prog.n_coef) + 2 * 8 * prog.n_slices * 10) + 2 * 16 * 4)
+    ubase = _ubuf_base(prog.n_coef, prog.n_slices)
     gi = prog.group_info.reshape(-1, 4)
     base = 0
     for g in range(prog.n_groups):
@@ -534,13 +748,13 @@ def emulate9(prog: HostProgram9, mats, inputs, inits, alpha, beta):
         q1 = int(gi[g + 1, 3])
         x = inputs[s]
         for q in range(q0, q1):
-            t = int(prog.step_rec[q])
+            t, sw = int(prog.step_rec[q]) & 0xFFFF, int(prog.step_rec[q]) >> 16
             for c in range(4):
                 for lane in range(32):
                     col = col0 + min(32 * c + lane, ncols - 1)
-                    ub[:, base + (q - q0) * GROUP_COLS + c * 32 + lane] = mats[t] @ x[:, col]
+                    ub[:, base + (q - q0) * GROUP_COLS + c * 32 + (lane ^ sw)] = mats[t] @ x[:, col]
         base += GROUP_COLS * (q1 - q0)
-    n_chunks = (prog.n_out_cols + 31) // 32
+    n_chunks = (len(prog.out_col) // 32) if prog.n_out_cols else 0
     meta = prog.gather_ptr.reshape(-1, 2)
     acc = np.zeros((n_rows, n_chunks * 32))
     for ch in range(n_chunks):
