@@ -167,7 +167,11 @@ typedef struct {
  * the previous one form a group of <= 32 rows solved by one CTA without a
  * global round trip per row.  L is passed as is (work_row[p] = p, io_row[p] =
  * source row of b, diag_inv = NULL); U is passed reversed (p = n-1-k,
- * work_row[p] = k, io_row[p] = destination row of x, diag_inv[p] = 1/U_kk).  */
+ * work_row[p] = k, io_row[p] = destination row of x, diag_inv[p] = 1/U_kk).
+ * The in-group block of every group is applied as a dense inverse:
+ * minv[minv_ptr[g] + r*gs + k] = ((D + B_g)^-1)[r][k] (gs = group size, B_g
+ * the strictly lower in-group entries, D = I for L and diag(U_kk) for U), so a
+ * group's rows are finished in parallel instead of by a sequential chain.    */
 typedef struct {
   int32_t n;
   int32_t n_groups;
@@ -186,6 +190,8 @@ typedef struct {
   const double* diag_inv;     /* [n] or NULL                               */
   int32_t* flags;             /* [n_groups * chunks] scratch               */
   int32_t* ticket;            /* [1] scratch                               */
+  const int64_t* minv_ptr;    /* [n_groups] offsets into minv              */
+  const double* minv;         /* dense in-group inverses, row-major gs x gs */
 } sgk_trigroups;
 
 /* Segmented row view: global row r lives in segment r / seg_rows.          */

@@ -102,7 +102,7 @@ class TriGroups(ctypes.Structure):
         ("n", c_i32), ("n_groups", c_i32), ("reversed", c_i32), ("pad", c_i32), ("rowptr", c_vp), ("split", c_vp), ("colind", c_vp), ("vals", c_vp),
         ("group_ptr", c_vp), ("group_order", c_vp), ("gdep_ptr", c_vp), ("gdep", c_vp), ("work_row", c_vp),
         ("io_row", c_vp),
-        ("diag_inv", c_vp), ("flags", c_vp), ("ticket", c_vp),
+        ("diag_inv", c_vp), ("flags", c_vp), ("ticket", c_vp), ("minv_ptr", c_vp), ("minv", c_vp),
     ]
 
 

@@ -25,16 +25,17 @@
 
 namespace sgk {
 
-__device__ __forceinline__ double seg_load(const sgk_segview& s, int r, int c) {
+// segment pointer by select, not by a dynamic index into the parameter array
+// (that copies the view to local memory: LDL round trips on the solve's
+// critical path)
+__device__ __forceinline__ double* seg_ptr(const sgk_segview& s, int r, int c) {
   const int seg = r / s.seg_rows;
   const int rr = r - seg * s.seg_rows;
-  return s.ptr[seg][(int64_t)rr * s.ld + s.col0 + c];
+  double* base = seg == 0 ? s.ptr[0] : (seg == 1 ? s.ptr[1] : s.ptr[2]);
+  return base + (int64_t)rr * s.ld + s.col0 + c;
 }
-__device__ __forceinline__ void seg_store(const sgk_segview& s, int r, int c, double v) {
-  const int seg = r / s.seg_rows;
-  const int rr = r - seg * s.seg_rows;
-  s.ptr[seg][(int64_t)rr * s.ld + s.col0 + c] = v;
-}
+__device__ __forceinline__ double seg_load(const sgk_segview& s, int r, int c) { return *seg_ptr(s, r, c); }
+__device__ __forceinline__ void seg_store(const sgk_segview& s, int r, int c, double v) { *seg_ptr(s, r, c) = v; }
 
 __device__ __forceinline__ void wait_flag(const int32_t* fl, int epoch) {
   if (ld_acquire(fl) == epoch) return;
@@ -184,12 +185,24 @@ __device__ __forceinline__ void load_cols(const double* __restrict__ p, double (
   }
 }
 
+#ifdef SGK_TRI_TRACE
+__device__ unsigned long long sgk_tri_trace[2][1 << 20][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRI_TR(k) do { if (tid == 0 && ticket < (1 << 20)) sgk_tri_trace[FWD ? 0 : 1][ticket][k] = gtimer(); } while (0)
+#else
+#define TRI_TR(k) do {} while (0)
+#endif
+
 template <bool FWD, int GCW, int GEPL>
-__global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview io, double* __restrict__ work,
+__global__ void __launch_bounds__(512, 2) trsv_group(sgk_trigroups t, sgk_segview io, double* __restrict__ work,
                                                   int width, int ldw, int n_chunks, int epoch) {
   __shared__ double part[GMAX][GCW];
   __shared__ double ys[GMAX][GCW];
-  __shared__ double lg[GMAX][GMAX + 1];  // dense in-group block (strictly lower)
+  __shared__ double lg[GMAX][GMAX + 1];  // dense inverse of the in-group block
   __shared__ int task_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -200,12 +213,29 @@ __global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview i
     const int ticket = task_s;
     __syncthreads();
     if (ticket >= n_tasks) return;
+    TRI_TR(0);
     const int gi = __ldg(t.group_order + ticket / n_chunks);
     const int chunk = ticket - (ticket / n_chunks) * n_chunks;
     const int r0 = __ldg(t.group_ptr + gi), r1 = __ldg(t.group_ptr + gi + 1);
     const int g = r1 - r0;
     const int c0 = chunk * GCW;
     const int w = min(GCW, width - c0);
+
+    // static data first (it does not depend on other groups, so its latency
+    // overlaps the wait): the group's dense inverse block and the right-hand
+    // side rows (b for L; for U the forward pass result, final at launch)
+    const int64_t mo = __ldg(t.minv_ptr + gi);
+    for (int i = tid; i < g * g; i += blockDim.x) {
+      const int r = i / g, k = i - r * g;
+      lg[r][k] = __ldg(t.minv + mo + i);
+    }
+    for (int i = tid; i < g * GCW; i += blockDim.x) {
+      const int r = i / GCW, c = i - r * GCW;
+      const int p = r0 + r;
+      part[r][c] = c >= w ? 0.0
+                          : FWD ? seg_load(io, __ldg(t.io_row + p), c0 + c)
+                                : __ldcg(work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + c);
+    }
 
     // 0: wait for the groups this group depends on (host-computed distinct
     //    dependency groups; one flag per (group, chunk))
@@ -218,15 +248,13 @@ __global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview i
       fence_acq_rel();
     }
     __syncthreads();
+    TRI_TR(1);
 
     // 1: outside contributions, rows over warps, lanes over entries
     for (int r = warp; r < g; r += nwarps) {
       const int p = r0 + r;
-      const int e0 = __ldg(t.rowptr + p), e2 = __ldg(t.rowptr + p + 1);
+      const int e0 = __ldg(t.rowptr + p);
       const int e1 = __ldg(t.split + p);  // first in-group entry (host-computed)
-      lg[r][lane] = 0.0;
-      __syncwarp();
-      if (lane < e2 - e1) lg[r][__ldg(t.colind + e1 + lane) - r0] = __ldg(t.vals + e1 + lane);
       double acc[GCW];
 #pragma unroll
       for (int c = 0; c < GCW; ++c) acc[c] = 0.0;
@@ -263,33 +291,26 @@ __global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview i
 #pragma unroll
         for (int c = 1; c < GCW; ++c)
           if (lane == c) s = acc[c];
-        const double init = FWD ? seg_load(io, __ldg(t.io_row + p), c0 + lane)
-                                : __ldcg(work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + lane);
-        part[r][lane] = init + s;
+        part[r][lane] += s;
       }
     }
     __syncthreads();
+    TRI_TR(2);
 
-    // 2: the in-group chain, one warp, right-looking: lane r holds row r's
-    //    partial sums; after row j is final its values are broadcast and every
-    //    later row subtracts L[r][j] * y_j (no global traffic, no barrier)
-    if (warp == 0) {
-      double pr[GCW];
-      const bool mine = lane < g;
+    // 2: the in-group block, y = (D + B)^-1 part: rows over warps, lanes over
+    //    the row's columns k <= r, one warp reduction per column
+    for (int r = warp; r < g; r += nwarps) {
+      const double m = lane <= r ? lg[r][lane] : 0.0;
 #pragma unroll
-      for (int c = 0; c < GCW; ++c) pr[c] = (mine && c < w) ? part[lane][c] : 0.0;
-      const double d = (!FWD && mine) ? __ldg(t.diag_inv + r0 + lane) : 1.0;
-      for (int j = 0; j < g; ++j) {
-        const double l = (lane > j && mine) ? lg[lane][j] : 0.0;
+      for (int c = 0; c < GCW; ++c) {
+        double v = lane <= r ? m * part[lane][c] : 0.0;
 #pragma unroll
-        for (int c = 0; c < GCW; ++c) {
-          const double yj = __shfl_sync(FULL, pr[c] * d, j);
-          if (lane == j) ys[j][c] = yj;
-          pr[c] = fma(-l, yj, pr[c]);
-        }
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (lane == 0) ys[r][c] = v;
       }
     }
     __syncthreads();
+    TRI_TR(3);
 
     // 3: write back (padded columns too: keeps the loads above unconditional),
     //    fence, publish the group flag for this chunk
@@ -302,6 +323,7 @@ __global__ void __launch_bounds__(512) trsv_group(sgk_trigroups t, sgk_segview i
     fence_acq_rel();
     __syncthreads();
     if (tid == 0) st_relaxed(t.flags + (int64_t)gi * n_chunks + chunk, epoch);
+    TRI_TR(4);
   }
 }
 
@@ -365,6 +387,13 @@ extern "C" int sgk_trisolve_grouped(const sgk_trigroups* L, const sgk_trigroups*
   if (L->n == 0 || width == 0) return SGK_OK;
   return launch_grouped(*L, *U, *b, *x, work, width, epoch, (cudaStream_t)stream);
 }
+
+#ifdef SGK_TRI_TRACE
+extern "C" int sgk_tri_trace_read(unsigned long long* out, int fwd, int n) {
+  return (int)cudaMemcpyFromSymbol(out, sgk::sgk_tri_trace, sizeof(unsigned long long) * 8 * (size_t)n,
+                                   fwd ? 0 : sizeof(unsigned long long) * 8 * (1 << 20));
+}
+#endif
 
 extern "C" int32_t sgk_trisolve_chunk_cols(void) { return sgk::CW; }
 extern "C" int32_t sgk_trisolve_grouped_chunk_cols(void) { return sgk::GCW_MIN; }

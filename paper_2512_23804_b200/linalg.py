@@ -16,6 +16,7 @@ import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
+from scipy.linalg import solve_triangular
 import scipy.linalg
 import scipy.sparse as sp
 import scipy.sparse.linalg
@@ -99,6 +100,23 @@ def group_dependencies(strict: csr_matrix, gptr: np.ndarray) -> tuple[np.ndarray
     return np.cumsum(ptr), dep
 
 
+def group_inverses(strict: csr_matrix, gptr: np.ndarray, dinv) -> tuple[np.ndarray, np.ndarray]:
+    """Dense inverse of each group's diagonal block (D + strictly lower
+    in-group entries; D = I, or 1/dinv for the reversed U), row-major, and the
+    offset of each group's block."""
+    ng = len(gptr) - 1
+    sizes = np.diff(gptr)
+    mptr = np.concatenate([[0], np.cumsum(sizes * sizes)]).astype(np.int64)
+    out = np.zeros(int(mptr[-1]))
+    for g in range(ng):
+        a, b = int(gptr[g]), int(gptr[g + 1])
+        m = b - a
+        blk = strict[a:b, a:b].toarray()
+        blk[np.arange(m), np.arange(m)] = 1.0 if dinv is None else 1.0 / np.asarray(dinv[a:b])
+        out[mptr[g]:mptr[g + 1]] = solve_triangular(blk, np.eye(m), lower=True).reshape(-1)
+    return mptr[:-1], out
+
+
 def chain_groups(strict: csr_matrix, max_rows: int = GROUP_MAX) -> tuple[np.ndarray, np.ndarray, int]:
     """Group consecutive rows of a strictly lower triangle into chains (row k
     joins the group of row k-1 when it depends on row k-1), and order the
@@ -156,6 +174,8 @@ def _grouped(strict: csr_matrix, work_row, io_row, dinv):
     ]
     dptr, deps = group_dependencies(strict, gptr)
     bufs += [_i32(dptr), _i32(deps if len(deps) else [0])]
+    mptr, minv = group_inverses(strict, gptr, dinv)
+    bufs += [torch.as_tensor(mptr, dtype=torch.int64).to(dev), _f64(minv if len(minv) else [0.0])]
     st = _lib.TriGroups(
         n=strict.shape[0], n_groups=len(gptr) - 1, reversed=int(n > 0 and work_row[0] != 0), pad=0, rowptr=bufs[0].data_ptr(), split=bufs[9].data_ptr(),
         colind=bufs[1].data_ptr(),
@@ -163,6 +183,7 @@ def _grouped(strict: csr_matrix, work_row, io_row, dinv):
         gdep_ptr=bufs[10].data_ptr(), gdep=bufs[11].data_ptr(),
         work_row=bufs[5].data_ptr(), io_row=bufs[6].data_ptr(),
         diag_inv=bufs[7].data_ptr() if bufs[7] is not None else None, flags=None, ticket=bufs[8].data_ptr(),
+        minv_ptr=bufs[12].data_ptr(), minv=bufs[13].data_ptr(),
     )
     return st, bufs, depth
 
