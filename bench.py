@@ -11,7 +11,9 @@ Headline line (one JSON object on rank 0):
     whole job over all ranks (weak scaling: each rank its own matvecs);
   * e2e = same metric through the public drop-in API `kron_apply` with V in
     pinned host memory: H2D(V) + kernel + D2H(W) inside the timed region;
-  * roofline = the fused program_kernel vs the measured HBM copy peak;
+  * roofline = the matvec kernel (stencil9_kernel on the Q1 pattern) vs the
+    measured HBM copy peak, plus its FP64 rate vs the measured DFMA peak (the
+    kernel's binding pipe: 7.9 GFLOP per matvec, SURVEY §7 H1);
   * cpu_baseline = the NumPy/SciPy oracle port of the reference path on a
     bounded row sample of the same workload, on this host;
   * solves = time-to-solution + iterations for config 2 (hGSoc-FGMRES and
@@ -37,6 +39,7 @@ from pathlib import Path
 import numpy as np
 
 ROOT = Path(__file__).resolve().parent
+FP64_PEAK_TFLOPS = 36.4  # measured DFMA peak on this pool's B200 (tools/fp64_probe.cu; DMMA 37.1)
 sys.path.insert(0, str(ROOT))
 
 SEED = 20240817
@@ -460,7 +463,7 @@ def run_ours(args):
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get("program_kernel_cfg4_bytes")
+            traffic = json.loads(tp.read_text()).get("matvec_kernel_cfg4_bytes")
         except Exception:
             traffic = None
     line = {
@@ -486,8 +489,9 @@ def run_ours(args):
                 "max_abs_diff_vs_device": e2e_err},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_kind": peak_kind, "kernel": "program_kernel (cfg4 full matvec)",
-                     "fp64_flops_per_launch": None},
+                     "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": ("stencil9_kernel" if prog.host.stats.get("mode") == "stencil9" else "program_kernel")
+                     + " (cfg4 full matvec)", "fp64_flops_per_launch": None},
         "clocks": clk.summary(),
     }
     prog_stats = prog.host.stats
@@ -496,6 +500,8 @@ def run_ours(args):
     useful = 2 * bundle.stiffness[0].nnz * prog_stats["n_products"] + 2 * bundle.n_h * prog_stats["n_gather"]
     line["roofline"]["fp64_flops_per_launch"] = useful
     line["roofline"]["fp64_tflops"] = useful / kernel_avg / 1e12
+    line["roofline"]["fp64_peak_tflops"] = FP64_PEAK_TFLOPS
+    line["roofline"]["fp64_frac"] = useful / kernel_avg / 1e12 / FP64_PEAK_TFLOPS
     if rank == 0 and not args.no_cpu:
         gbs, dt, rows, b = cpu_sample(bundle, x_host, budget_s=args.ref_budget)
         line["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "port",

@@ -187,6 +187,7 @@ __device__ __forceinline__ void load_cols(const double* __restrict__ p, double (
 
 #ifdef SGK_TRI_TRACE
 __device__ unsigned long long sgk_tri_trace[2][1 << 20][8];
+__device__ int sgk_tri_bad[2];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -249,6 +250,15 @@ __global__ void __launch_bounds__(512, 2) trsv_group(sgk_trigroups t, sgk_segvie
     }
     __syncthreads();
     TRI_TR(1);
+#ifdef SGK_TRI_TRACE
+    if (tid == 0) {
+      const int da = __ldg(t.gdep_ptr + gi), db = __ldg(t.gdep_ptr + gi + 1);
+      int bad = 0;
+      for (int d = da; d < db; ++d)
+        bad += ld_relaxed(t.flags + (int64_t)__ldg(t.gdep + d) * n_chunks + chunk) != epoch;
+      if (bad) atomicAdd(&sgk_tri_bad[FWD ? 0 : 1], 1);
+    }
+#endif
 
     // 1: outside contributions, rows over warps, lanes over entries
     for (int r = warp; r < g; r += nwarps) {
@@ -389,6 +399,7 @@ extern "C" int sgk_trisolve_grouped(const sgk_trigroups* L, const sgk_trigroups*
 }
 
 #ifdef SGK_TRI_TRACE
+extern "C" int sgk_tri_bad_read(int* out) { return (int)cudaMemcpyFromSymbol(out, sgk::sgk_tri_bad, 2 * sizeof(int)); }
 extern "C" int sgk_tri_trace_read(unsigned long long* out, int fwd, int n) {
   return (int)cudaMemcpyFromSymbol(out, sgk::sgk_tri_trace, sizeof(unsigned long long) * 8 * (size_t)n,
                                    fwd ? 0 : sizeof(unsigned long long) * 8 * (1 << 20));

@@ -21,6 +21,9 @@ for _ in range(3):
     fac.solve_segments([(t, lo) for t in blk], [(t, lo) for t in out], hi - lo)
 torch.cuda.synchronize()
 lib = _lib.lib()
+bad = (ctypes.c_int * 2)()
+lib.sgk_tri_bad_read(bad)
+print("tasks that passed the dependency wait with an unset flag (fwd, bwd):", bad[0], bad[1])
 for fwd, bufs, gs in ((1, fac.gl_bufs, fac.gl), (0, fac.gu_bufs, fac.gu)):
     ng = gs.n_groups
     width = hi - lo
@@ -49,3 +52,28 @@ for fwd, bufs, gs in ((1, fac.gl_bufs, fac.gl), (0, fac.gu_bufs, fac.gu)):
     f = lambda a: f"{np.median(a)/1e3:.2f}/{np.mean(a)/1e3:.2f}"
     print(f"{'L' if fwd else 'U'} width {width} groups {ng} tasks {nt} total {done.max()/1e3:.0f} us; median/mean us: "
           f"notify {f(notif)} phase1 {f(ph1)} chain {f(ph2)} [setup {c5/1e3:.2f} loop {c6/1e3:.2f} sync {c7/1e3:.2f}] write+fence {f(ph3)} wait {f(wait)}")
+    if fwd and nch == 1:
+        rp = bufs[0].cpu().numpy(); sp_ = bufs[9].cpu().numpy(); gp = bufs[3].cpu().numpy()
+        ph1a = np.array(ph1)
+        top = np.argsort(-ph1a)[:12]
+        print("  top phase-1 tasks (ticket, rows, outside entries, phase1 us, done us):")
+        for tk in top:
+            g = order[tk]
+            a, b_ = gp[g], gp[g + 1]
+            ne = int((sp_[a:b_] - rp[a:b_]).sum())
+            print(f"   {tk:5d} rows {b_ - a:2d} entries {ne:7d} phase1 {ph1a[tk]/1e3:8.1f} done {done[tk]/1e3:8.1f}")
+        # critical path walk back from the last task
+        cp, tk = [], int(np.argmax(done))
+        while True:
+            g = order[tk]; cp.append(tk)
+            ds = deps[dptr[g]:dptr[g + 1]]
+            if not len(ds): break
+            tk = int(max((pos[d] for d in ds), key=lambda q: done[q]))
+        cp = cp[::-1]
+        tot1 = sum(ph1a[q] for q in cp)
+        print(f"  critical path: {len(cp)} tasks, sum phase1 {tot1/1e3:.0f} us, end {done.max()/1e3:.0f} us")
+        for tk in (4377, 4376, 4375):
+            if tk >= nt: continue
+            g = order[tk]; ds = deps[dptr[g]:dptr[g + 1]]
+            dd = sorted(((done[pos[d]], pos[d]) for d in ds), reverse=True)[:3]
+            print(f"  task {tk} group {g}: t0..t4 {[round(x/1e3,1) for x in tr[tk,:5]]} n_deps {len(ds)} latest deps (done, ticket) {[(round(a/1e3,1), int(b)) for a, b in dd]}")
