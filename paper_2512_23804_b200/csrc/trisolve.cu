@@ -168,6 +168,9 @@ static int launch_chunked(const sgk_trifactor& L, const sgk_trifactor& U, const 
 // The triangle is given in "processing space" (rows in dependency order,
 // strictly lower); the U factor is passed reversed.
 constexpr int GMAX = 32;
+#ifndef SGK_TRI_EPL_NARROW
+#define SGK_TRI_EPL_NARROW 16  // entries per lane per batch for 1-2 column chunks
+#endif
 constexpr int GCW_MIN = 1;  // narrowest grouped chunk (sizes the flag array)
 
 template <int GCW>
@@ -375,8 +378,8 @@ static int launch_grouped(const sgk_trigroups& L, const sgk_trigroups& U, const 
   const int threads = env_int("SGKKT_TRI_THREADS", width > 200 ? 256 : 512);
   const int occ_cap = env_int("SGKKT_TRI_OCC", width > 200 ? 4 : 2);
   const int epl = env_int("SGKKT_TRI_EPL", 8);
-  if (cw <= 1) return launch_grouped_t<1, 16>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
-  if (cw <= 2) return launch_grouped_t<2, 16>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
+  if (cw <= 1) return launch_grouped_t<1, SGK_TRI_EPL_NARROW>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
+  if (cw <= 2) return launch_grouped_t<2, SGK_TRI_EPL_NARROW>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
   if (cw <= 4 && epl >= 16) return launch_grouped_t<4, 16>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
   if (cw <= 4) return launch_grouped_t<4, 8>(L, U, b, x, work, width, epoch, threads, occ_cap, st);
   if (cw <= 8) return launch_grouped_t<8, 4>(L, U, b, x, work, width, epoch, threads, occ_cap, st);

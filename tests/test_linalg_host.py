@@ -135,3 +135,67 @@ def test_grouped_trisolve_emulation(rng, kind):
     want = lu.solve(rhs)
     got = emulate_grouped(lu, rhs)
     assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def emulate_group_blocks(strict, dinv, gptr, order, mptr, minv, rhs):
+    """NumPy emulation of trsv_group on a processing-space lower triangle:
+    groups in ticket order, outside contributions, then the dense in-group
+    inverse block (csrc/trisolve.cu phases 1-2)."""
+    n = strict.shape[0]
+    y = np.full_like(rhs, np.nan)
+    for g in order:
+        a, b = int(gptr[g]), int(gptr[g + 1])
+        part = rhs[a:b].copy()
+        for r in range(a, b):
+            lo, hi = strict.indptr[r], strict.indptr[r + 1]
+            cols, vals = strict.indices[lo:hi], strict.data[lo:hi]
+            out = cols < a
+            assert not np.isnan(y[cols[out]]).any(), "dependency not finished"
+            part[r - a] -= vals[out] @ y[cols[out]]
+        m = b - a
+        blk = minv[mptr[g]:mptr[g] + m * m].reshape(m, m)
+        y[a:b] = blk @ part
+    return y
+
+
+@pytest.mark.parametrize("upper", [False, True])
+def test_grouped_inverse_blocks_solve_the_triangle(rng, upper):
+    from paper_2512_23804_b200.linalg import chain_groups, group_dependencies, group_inverses
+
+    b = build_problem(2, n=8)
+    s = steady_system(b)
+    a = sp.bmat([[s.mass, None, -s.stiffness[0]], [None, s.beta * s.mass, s.mass],
+                 [-s.stiffness[0], s.mass, None]], format="csr")
+    lu = spla.splu(sp.csc_matrix(a), diag_pivot_thresh=1.0)
+    if upper:  # U reversed into a lower triangle, as grouped_triangles does
+        u = sp.csr_matrix(lu.U)
+        n = u.shape[0]
+        rev = np.arange(n)[::-1]
+        t = sp.csr_matrix(u.toarray()[np.ix_(rev, rev)])
+        dinv = 1.0 / t.diagonal()
+        strict = sp.tril(t, k=-1, format="csr")
+        full = t
+    else:
+        strict = sp.tril(sp.csr_matrix(lu.L), k=-1, format="csr")
+        dinv = None
+        full = strict + sp.eye(strict.shape[0], format="csr")
+    strict.sort_indices()
+    gptr, order, depth = chain_groups(strict)
+    assert gptr[0] == 0 and gptr[-1] == strict.shape[0] and np.diff(gptr).max() <= 32
+    # every row of a group after its first depends on the previous row
+    for g in range(len(gptr) - 1):
+        for r in range(gptr[g] + 1, gptr[g + 1]):
+            assert (r - 1) in strict.indices[strict.indptr[r]:strict.indptr[r + 1]]
+    dptr, deps = group_dependencies(strict, gptr)
+    gid = np.repeat(np.arange(len(gptr) - 1), np.diff(gptr))
+    for g in range(len(gptr) - 1):
+        rows = range(gptr[g], gptr[g + 1])
+        want = set()
+        for r in rows:
+            cols = strict.indices[strict.indptr[r]:strict.indptr[r + 1]]
+            want |= set(gid[cols[cols < gptr[g]]].tolist())
+        assert set(deps[dptr[g]:dptr[g + 1]].tolist()) == want
+    mptr, minv = group_inverses(strict, gptr, dinv)
+    rhs = rng.standard_normal((strict.shape[0], 2))
+    y = emulate_group_blocks(strict, dinv, gptr, order, mptr, minv, rhs)
+    assert np.abs(full @ y - rhs).max() <= 1e-10 * np.abs(rhs).max()

@@ -77,3 +77,9 @@ for fwd, bufs, gs in ((1, fac.gl_bufs, fac.gl), (0, fac.gu_bufs, fac.gu)):
             g = order[tk]; ds = deps[dptr[g]:dptr[g + 1]]
             dd = sorted(((done[pos[d]], pos[d]) for d in ds), reverse=True)[:3]
             print(f"  task {tk} group {g}: t0..t4 {[round(x/1e3,1) for x in tr[tk,:5]]} n_deps {len(ds)} latest deps (done, ticket) {[(round(a/1e3,1), int(b)) for a, b in dd]}")
+    fin = np.sort(done)
+    q = [fin[int(f * (len(fin) - 1))] / 1e3 for f in (0.5, 0.9, 0.99, 1.0)]
+    grp_done = np.array([done[pos[g] * nch:(pos[g] + 1) * nch].max() for g in range(ng)])
+    last = np.argsort(grp_done)[-40:]
+    print(f"  task completion quantiles (us): 50% {q[0]:.0f}  90% {q[1]:.0f}  99% {q[2]:.0f}  100% {q[3]:.0f};"
+          f" last 40 groups finish between {grp_done[last].min()/1e3:.0f} and {grp_done.max()/1e3:.0f} us")
