@@ -192,6 +192,15 @@ typedef struct {
   int32_t* ticket;            /* [1] scratch                               */
   const int64_t* minv_ptr;    /* [n_groups] offsets into minv              */
   const double* minv;         /* dense in-group inverses, row-major gs x gs */
+  /* dense region: groups [dense_g0, dense_g0+dense_nb) are 32-row blocks of
+   * rows dense_r0.. whose off-diagonal blocks against earlier region rows are
+   * stored densely (block i: 32 x 32i row-major at dense + 1024*i*(i-1)/2)
+   * and streamed block by block as the earlier blocks finish             */
+  int32_t dense_g0;
+  int32_t dense_nb;
+  int32_t dense_r0;
+  int32_t dense_pad;
+  const double* dense;
 } sgk_trigroups;
 
 /* Segmented row view: global row r lives in segment r / seg_rows.          */

@@ -103,6 +103,7 @@ class TriGroups(ctypes.Structure):
         ("group_ptr", c_vp), ("group_order", c_vp), ("gdep_ptr", c_vp), ("gdep", c_vp), ("work_row", c_vp),
         ("io_row", c_vp),
         ("diag_inv", c_vp), ("flags", c_vp), ("ticket", c_vp), ("minv_ptr", c_vp), ("minv", c_vp),
+        ("dense_g0", c_i32), ("dense_nb", c_i32), ("dense_r0", c_i32), ("dense_pad", c_i32), ("dense", c_vp),
     ]
 
 

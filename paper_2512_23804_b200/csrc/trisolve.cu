@@ -307,6 +307,64 @@ __global__ void __launch_bounds__(512, 2) trsv_group(sgk_trigroups t, sgk_segvie
         part[r][lane] += s;
       }
     }
+
+    // 1b: dense region block: stream the earlier region blocks as they finish
+    //     (lane k polls block j+k; every ready prefix is consumed at once), a
+    //     warp per row, lanes over the 32 columns of a block; the per-lane
+    //     partial sums are reduced once at the end
+    if ((unsigned)(gi - t.dense_g0) < (unsigned)t.dense_nb) {
+      const int bi = gi - t.dense_g0;
+      const int ldd = GMAX * bi;
+      const double* D = t.dense + (int64_t)GMAX * GMAX * bi * (bi - 1) / 2;
+      constexpr int RPW = 2;  // rows per warp and pass (one pass with 16 warps)
+      for (int rb = 0; rb < g; rb += RPW * nwarps) {
+        double dacc[RPW][GCW];
+#pragma unroll
+        for (int q = 0; q < RPW; ++q)
+#pragma unroll
+          for (int c = 0; c < GCW; ++c) dacc[q][c] = 0.0;
+        int j = 0;
+        while (j < bi) {
+          const bool mine = lane < bi - j;
+          const int v = mine ? ld_relaxed(t.flags + (int64_t)(t.dense_g0 + j + lane) * n_chunks + chunk) : epoch;
+          const unsigned notready = __ballot_sync(FULL, v != epoch);
+          const int ready = notready ? __ffs(notready) - 1 : min(32, bi - j);
+          if (ready == 0) {
+            __nanosleep(64);
+            continue;
+          }
+          fence_acq_rel();
+          __syncwarp();
+          for (int jj = j; jj < j + ready; ++jj) {
+            const int src = t.dense_r0 + GMAX * jj + lane;  // processing row of this lane's column
+            const int wr = t.reversed ? t.n - 1 - src : src;
+            double xv[GCW];
+            load_cols<GCW>(work + (int64_t)wr * ldw + c0, xv);
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) {
+              const int r = rb + warp + q * nwarps;
+              if (r < g) {
+                const double d = __ldg(D + (int64_t)r * ldd + GMAX * jj + lane);
+#pragma unroll
+                for (int c = 0; c < GCW; ++c) dacc[q][c] = fma(d, xv[c], dacc[q][c]);
+              }
+            }
+          }
+          j += ready;
+        }
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+          const int r = rb + warp + q * nwarps;
+#pragma unroll
+          for (int c = 0; c < GCW; ++c) {
+            double a = dacc[q][c];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(FULL, a, o);
+            if (r < g && lane == c) part[r][c] -= a;
+          }
+        }
+      }
+    }
     __syncthreads();
     TRI_TR(2);
 

@@ -81,6 +81,7 @@ def level_schedule(strict: csr_matrix, lower: bool) -> tuple[np.ndarray, int]:
 GROUP_MAX = 32
 # SGKKT_TRISOLVE=rows selects the row-granular kernel (A/B testing)
 GROUPED = __import__("os").environ.get("SGKKT_TRISOLVE", "grouped") != "rows"
+DENSE = __import__("os").environ.get("SGKKT_TRI_DENSE", "1") != "0"  # dense-region streaming (grouped solve)
 
 
 def group_dependencies(strict: csr_matrix, gptr: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
@@ -117,16 +118,45 @@ def group_inverses(strict: csr_matrix, gptr: np.ndarray, dinv) -> tuple[np.ndarr
     return mptr[:-1], out
 
 
-def chain_groups(strict: csr_matrix, max_rows: int = GROUP_MAX) -> tuple[np.ndarray, np.ndarray, int]:
+DENSE_BLOCK = 32  # rows per block of a dense region (= GMAX in csrc/trisolve.cu)
+DENSE_MIN_DENSITY = 0.5
+DENSE_SIZES = (128, 256, 384, 512, 768, 1024, 1536, 2048, 2560, 3072, 4096)
+
+
+def dense_region(strict: csr_matrix) -> tuple[int, int]:
+    """Rows [r0, r1) of a strictly lower triangle whose diagonal block is
+    nearly dense: the trailing block of L or the leading block of the
+    reversed U (the separator rows COLAMD puts last fill in).  Largest
+    candidate size with density >= DENSE_MIN_DENSITY, else an empty region."""
+    n = strict.shape[0]
+    best = (0, 0)
+    for m in DENSE_SIZES:
+        if m > n // 2:
+            break
+        for r0 in (n - m, 0):
+            blk = strict[r0:r0 + m, r0:r0 + m]
+            if blk.nnz >= DENSE_MIN_DENSITY * m * (m - 1) / 2 and m > best[1] - best[0]:
+                best = (r0, r0 + m)
+    return best
+
+
+def chain_groups(strict: csr_matrix, max_rows: int = GROUP_MAX,
+                 dense: tuple[int, int] = (0, 0)) -> tuple[np.ndarray, np.ndarray, int]:
     """Group consecutive rows of a strictly lower triangle into chains (row k
-    joins the group of row k-1 when it depends on row k-1), and order the
-    groups topologically by group level.  Returns (group_ptr, order, depth)."""
+    joins the group of row k-1 when it depends on row k-1); the rows of a
+    dense region form fixed blocks of DENSE_BLOCK rows.  Groups are ordered
+    topologically by group level.  Returns (group_ptr, order, depth)."""
     n = strict.shape[0]
     ip, ix = strict.indptr, strict.indices
+    d0, d1 = dense
     starts = [0]
     for k in range(1, n):
+        if d0 <= k < d1:
+            if (k - d0) % DENSE_BLOCK == 0:
+                starts.append(k)
+            continue
         dep_prev = ip[k + 1] > ip[k] and ix[ip[k + 1] - 1] == k - 1
-        if not dep_prev or k - starts[-1] >= max_rows:
+        if not dep_prev or k - starts[-1] >= max_rows or k == d1:
             starts.append(k)
     gptr = np.array(starts + [n], dtype=np.int64) if n else np.zeros(1, np.int64)
     ng = len(gptr) - 1
@@ -155,11 +185,30 @@ def grouped_triangles(l_strict, u_strict, diag, in_perm, out_perm):
     return (l_strict, np.arange(n), np.asarray(in_perm), None), (u_rev, rev, np.asarray(out_perm)[rev], 1.0 / diag[rev])
 
 
+def dense_blocks(strict: csr_matrix, dense: tuple[int, int]) -> np.ndarray:
+    """Row-major dense copies of the dense region's off-diagonal blocks: block
+    i (rows d0+32i ..) against columns [d0, d0+32i), offsets 1024*i*(i-1)/2."""
+    d0, d1 = dense
+    nb = (d1 - d0) // DENSE_BLOCK
+    out = np.zeros(DENSE_BLOCK * DENSE_BLOCK * nb * (nb - 1) // 2) if nb else np.zeros(1)
+    for i in range(1, nb):
+        a = d0 + DENSE_BLOCK * i
+        blk = strict[a:a + DENSE_BLOCK, d0:a].toarray()
+        off = DENSE_BLOCK * DENSE_BLOCK * i * (i - 1) // 2
+        out[off:off + blk.size] = blk.reshape(-1)
+    return out
+
+
 def _grouped(strict: csr_matrix, work_row, io_row, dinv):
-    gptr, order, depth = chain_groups(strict)
     n = strict.shape[0]
+    dense = dense_region(strict) if DENSE else (0, 0)
+    gptr, order, depth = chain_groups(strict, dense=dense)
     # first entry of each row whose column lies inside the row's own group
+    # (dense-region rows: inside the region; the region's off-diagonal blocks
+    # are applied from dense copies, streamed block by block)
     gstart = np.repeat(gptr[:-1], np.diff(gptr)) if n else np.zeros(0, np.int64)
+    if dense[1] > dense[0]:
+        gstart[dense[0]:dense[1]] = dense[0]
     row_of = np.repeat(np.arange(n), np.diff(strict.indptr))
     inside = strict.indices >= gstart[row_of] if strict.nnz else np.zeros(0, bool)
     split = strict.indptr[1:] - np.bincount(row_of[inside], minlength=n) if n else np.zeros(0, np.int64)
@@ -173,9 +222,21 @@ def _grouped(strict: csr_matrix, work_row, io_row, dinv):
         _i32(split if n else [0]),
     ]
     dptr, deps = group_dependencies(strict, gptr)
+    ng = len(gptr) - 1
+    dg0 = int(np.searchsorted(gptr, dense[0])) if dense[1] > dense[0] else ng
+    nb = (dense[1] - dense[0]) // DENSE_BLOCK
+    if nb:  # a dense block waits only for its sparse dependencies up front
+        keep = np.ones(len(deps), bool)
+        for g in range(dg0, dg0 + nb):
+            seg = slice(dptr[g], dptr[g + 1])
+            keep[seg] = (deps[seg] < dg0) | (deps[seg] >= dg0 + nb)
+        owner = np.repeat(np.arange(ng), np.diff(dptr))
+        deps = deps[keep]
+        dptr = np.concatenate([[0], np.cumsum(np.bincount(owner[keep], minlength=ng))])
     bufs += [_i32(dptr), _i32(deps if len(deps) else [0])]
     mptr, minv = group_inverses(strict, gptr, dinv)
     bufs += [torch.as_tensor(mptr, dtype=torch.int64).to(dev), _f64(minv if len(minv) else [0.0])]
+    bufs += [_f64(dense_blocks(strict, dense))]
     st = _lib.TriGroups(
         n=strict.shape[0], n_groups=len(gptr) - 1, reversed=int(n > 0 and work_row[0] != 0), pad=0, rowptr=bufs[0].data_ptr(), split=bufs[9].data_ptr(),
         colind=bufs[1].data_ptr(),
@@ -184,6 +245,7 @@ def _grouped(strict: csr_matrix, work_row, io_row, dinv):
         work_row=bufs[5].data_ptr(), io_row=bufs[6].data_ptr(),
         diag_inv=bufs[7].data_ptr() if bufs[7] is not None else None, flags=None, ticket=bufs[8].data_ptr(),
         minv_ptr=bufs[12].data_ptr(), minv=bufs[13].data_ptr(),
+        dense_g0=dg0, dense_nb=nb, dense_r0=dense[0], dense_pad=0, dense=bufs[14].data_ptr(),
     )
     return st, bufs, depth
 

@@ -246,3 +246,34 @@ def test_pinned_host_pipeline_matches_device_path():
     want = kron_apply(op, x.cuda()).cpu()
     assert got is out
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("dense", [True, False])
+def test_ptilde_solve_all_chunk_paths_vs_superlu(dense, monkeypatch):
+    """The grouped triangular solve through every chunk width / CTA shape
+    (1, 2, 4 columns; 512- and 256-thread CTAs above width 200) and with /
+    without the dense-region streaming, against SuperLU on the same P~."""
+    import scipy.sparse.linalg as spla
+    import torch
+
+    from paper_2512_23804_b200 import linalg
+    from paper_2512_23804_b200.preconditioners import deterministic_kkt_matrix
+
+    monkeypatch.setattr(linalg, "DENSE", dense)
+    b, sys_ = _control(5, n=32)
+    k = deterministic_kkt_matrix(sys_).tocsc()
+    lu = spla.splu(k, diag_pivot_thresh=1.0)
+    fac = linalg.TriangularFactors.from_superlu(lu)
+    if dense:
+        assert fac.gl.dense_nb > 0 and fac.gu.dense_nb > 0
+    n = k.shape[0] // 3
+    rng = np.random.default_rng(7)
+    for width in (1, 7, 33, 250):
+        rhs = rng.standard_normal((3 * n, width))
+        want = lu.solve(rhs)
+        segs = [torch.as_tensor(np.ascontiguousarray(rhs[i * n:(i + 1) * n])).cuda() for i in range(3)]
+        outs = [torch.empty_like(s) for s in segs]
+        fac.solve_segments([(s, 0) for s in segs], [(o, 0) for o in outs], width)
+        got = np.concatenate([o.cpu().numpy() for o in outs])
+        err = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert err <= 1e-11, (width, err)

@@ -199,3 +199,30 @@ def test_grouped_inverse_blocks_solve_the_triangle(rng, upper):
     rhs = rng.standard_normal((strict.shape[0], 2))
     y = emulate_group_blocks(strict, dinv, gptr, order, mptr, minv, rhs)
     assert np.abs(full @ y - rhs).max() <= 1e-10 * np.abs(rhs).max()
+
+
+def test_dense_region_blocks_reproduce_the_factor():
+    from paper_2512_23804_b200.linalg import DENSE_BLOCK, chain_groups, dense_blocks, dense_region
+
+    b = build_problem(2, n=16)
+    s = steady_system(b)
+    a = sp.bmat([[s.mass, None, -s.stiffness[0]], [None, s.beta * s.mass, s.mass],
+                 [-s.stiffness[0], s.mass, None]], format="csr")
+    lu = spla.splu(sp.csc_matrix(a), diag_pivot_thresh=1.0)
+    strict = sp.tril(sp.csr_matrix(lu.L), k=-1, format="csr")
+    strict.sort_indices()
+    d0, d1 = dense_region(strict)
+    assert d1 - d0 >= 128 and (d1 - d0) % DENSE_BLOCK == 0 and d1 == strict.shape[0]
+    blk = strict[d0:d1, d0:d1]
+    assert blk.nnz >= 0.5 * (d1 - d0) * (d1 - d0 - 1) / 2
+    gptr, order, _ = chain_groups(strict, dense=(d0, d1))
+    starts = set(gptr.tolist())
+    assert all(r in starts for r in range(d0, d1, DENSE_BLOCK))
+    assert not any(d0 < r < d1 and (r - d0) % DENSE_BLOCK for r in starts)
+    dense = dense_blocks(strict, (d0, d1))
+    full = strict.toarray()
+    for i in range(1, (d1 - d0) // DENSE_BLOCK):
+        r = d0 + DENSE_BLOCK * i
+        off = DENSE_BLOCK * DENSE_BLOCK * i * (i - 1) // 2
+        got = dense[off:off + DENSE_BLOCK * DENSE_BLOCK * i].reshape(DENSE_BLOCK, DENSE_BLOCK * i)
+        assert np.array_equal(got, full[r:r + DENSE_BLOCK, d0:r])
