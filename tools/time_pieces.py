@@ -52,3 +52,9 @@ lead = bd.sweep.lead_factor.device_factors
 print(f"A~ factor+upload {time.time() - t0:.1f}s nnzL={lead.nnz_l} depthL={lead.depth_l} depthU={lead.depth_u}", flush=True)
 print(f"blockdiag apply {timed(lambda: bd.apply_device(*blocks, outs=outs), reps=2):.3f} ms", flush=True)
 print(f"hgs sweep {timed(lambda: bd.sweep.apply_device(blocks[2]), reps=2):.3f} ms", flush=True)
+cheb = bd.mass_solve if hasattr(bd, "mass_solve") else None
+for lo, hi in b.partition.ranges():
+    segs = [(blocks[0], lo)]
+    o2 = [(outs[0], lo)]
+    print(f"  A~ solve width {hi - lo}: {timed(lambda: lead.solve_segments(segs, o2, hi - lo), reps=2):.3f} ms", flush=True)
+print(f"  A~ dense regions: L {lead.gl.dense_nb} blocks, U {lead.gu.dense_nb} blocks; groups L/U {lead.gl.n_groups}/{lead.gu.n_groups}")
