@@ -8,7 +8,7 @@ LIB := paper_2512_23804_b200/libsgkkt_b200.so
 all: $(LIB)
 
 $(LIB): $(SRC) paper_2512_23804_b200/csrc/sgk_common.cuh include/sgkkt_b200.h
-	$(NVCC) $(ARCH) $(NVFLAGS) -shared -o $@ $(SRC)
+	$(NVCC) $(ARCH) $(NVFLAGS) -shared -o $@ $(SRC) -lcublas -Xlinker -rpath,/usr/local/cuda/lib64
 
 ptxas:
 	$(NVCC) $(ARCH) $(NVFLAGS) -Xptxas -v -c -o /tmp/sgk_probe.o paper_2512_23804_b200/csrc/galerkin.cu

@@ -263,9 +263,12 @@ def _event_time(fn, steps, stream):
     return start.elapsed_time(end) / 1e3
 
 
-def solve_block(cfg_id, betas, with_cpu=False):
+def solve_block(cfg_id, betas, with_cpu=False, lead_solvers=("lu", "fastdiag")):
     """Time-to-solution of the control configs on the GPU (setup reported
-    separately)."""
+    separately).  Lead solvers: "lu" = the reference's SuperLU factors replayed
+    by the GPU triangular solves (the reference algorithm); "fastdiag" = the
+    depth-free Kronecker-sum solve, keys suffixed
+    "[fastdiag]"."""
     import torch
 
     from paper_2512_23804_b200.krylov import FgmresConfig, fgmres, minres
@@ -294,10 +297,15 @@ def solve_block(cfg_id, betas, with_cpu=False):
             return o
 
         rec = {}
-        for name, builder, solver in (
-            ("hgsoc_fgmres", lambda: build_coupled_preconditioner(sys_, bundle.partition), fgmres),
-            ("blockdiag_hgs_minres", lambda: build_steady_preconditioner(sys_, bundle.partition, "cheb5"), minres),
-        ):
+        variants = []
+        for ls in lead_solvers:
+            sfx = "" if ls == "lu" else f"[{ls}]"
+            variants.append((f"hgsoc_fgmres{sfx}",
+                             lambda ls=ls: build_coupled_preconditioner(sys_, bundle.partition, lead_solver=ls), fgmres))
+            variants.append((f"blockdiag_hgs_minres{sfx}",
+                             lambda ls=ls: build_steady_preconditioner(sys_, bundle.partition, "cheb5", lead_solver=ls),
+                             minres))
+        for name, builder, solver in variants:
             t0 = time.perf_counter()
             prec = builder()
             # first apply compiles programs and uploads factors (setup)
@@ -509,7 +517,7 @@ def run_ours(args):
                                           f"{dt:.2f} s); NumPy/SciPy oracle port of sgkkt kron_apply, 1 core (GIL-bound)"}
     if rank == 0 and not args.no_solve:
         solves = {"cfg2": solve_block(2, [1e-2])}
-        if args.solve_cfg5:
+        if not args.no_solve_cfg5:
             solves["cfg5"] = solve_block(5, [1e-2, 1e-4, 1e-6])
         if args.solve_time:
             solves["time_dependent"] = time_solve_block(args.time_cpu)
@@ -528,7 +536,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
-    ap.add_argument("--solve-cfg5", action="store_true")
+    ap.add_argument("--solve-cfg5", action="store_true", help="(default on; kept for compatibility)")
+    ap.add_argument("--no-solve-cfg5", action="store_true", help="skip the cfg5 beta sweep")
     ap.add_argument("--solve-time", action="store_true", help="time-dependent PINT solve (SURVEY 8(f) row 1)")
     ap.add_argument("--time-cpu", action="store_true", help="also time the CPU port of the time-dependent solve")
     ap.add_argument("--ref-budget", type=float, default=3.0)

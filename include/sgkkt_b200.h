@@ -20,6 +20,8 @@
  *   sgk_trisolve           linalg.py:76-87      LUFactors.solve (SuperLU gstrs),
  *                          applied to all columns of one degree level at once
  *                          (preconditioners.py:155-164, 422-433)
+ *   sgk_fastdiag_solve     linalg.py:76-87      LUFactors.solve for a Kronecker-sum lead
+ *                          (A_1, A_1 + c M, and the P~ block of preconditioners.py:437-448)
  *   sgk_cheb_step          preconditioners.py:70-98  chebyshev_mass_solve (one step)
  *   sgk_colscale           preconditioners.py:248-255 (column weights h^gamma, 1/beta)
  *   sgk_dot_partial,
@@ -229,6 +231,29 @@ int32_t sgk_trisolve_grouped_chunk_cols(void);
 int sgk_trisolve_grouped(const sgk_trigroups* L, const sgk_trigroups* U,
                          const sgk_segview* b, const sgk_segview* x,
                          double* work, int32_t width, int32_t epoch, void* stream);
+
+/* Fast-diagonalisation factor of a Kronecker-sum lead (
+ * replaces LUFactors.solve, linalg.py:76-87, when the lead is
+ * A = K1(x)M1 + M1(x)K1 on an n x n tensor grid and M = M1(x)M1):
+ * s  = S   (n x n row-major, K1 S = M1 S diag(mu), S^T M1 S = I),
+ * st = S^T (n x n row-major), lam[a*n+b] = mu_a + mu_b.
+ * n_seg == 1: X = A^-1 B.  n_seg == 3: the hGSoc block
+ * P~ = [M 0 -A; 0 beta M M; -A M 0] (preconditioners.py:437-448) on the
+ * (y, u, lambda) segments.  The four dense passes are cuBLAS DGEMMs; the
+ * modal solve is this library's kernel.  work: sgk_fastdiag_work_doubles()
+ * doubles.  B and X may alias.                                              */
+typedef struct {
+  int32_t n;
+  int32_t n_seg;
+  const double* s;
+  const double* st;
+  const double* lam;
+  double beta;
+} sgk_fastdiag;
+int64_t sgk_fastdiag_work_doubles(const sgk_fastdiag* fd, int32_t width);
+int sgk_fastdiag_solve(const sgk_fastdiag* fd, const sgk_segview* b,
+                       const sgk_segview* x, double* work, int32_t width,
+                       void* stream);
 
 /* One Chebyshev semi-iteration step on all columns (preconditioners.py:89-97):
  * x_new = omega*(scale .* (b - M x) + x - x_prev) + x_prev,

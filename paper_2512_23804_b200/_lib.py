@@ -20,6 +20,7 @@ __all__ = [
     "View",
     "TriFactor",
     "SegView",
+    "FastDiag",
     "stream_ptr",
     "library_path",
     "launch_count",
@@ -111,6 +112,10 @@ class SegView(ctypes.Structure):
     _fields_ = [("ptr", c_vp * 3), ("ld", c_i64), ("col0", c_i32), ("seg_rows", c_i32)]
 
 
+class FastDiag(ctypes.Structure):
+    _fields_ = [("n", c_i32), ("n_seg", c_i32), ("s", c_vp), ("st", c_vp), ("lam", c_vp), ("beta", c_dbl)]
+
+
 _SIGNATURES = {
     "sgk_program_apply": (c_i32, [ctypes.POINTER(Pattern), ctypes.POINTER(Program), c_i32,
                                   ctypes.POINTER(View), c_i32, ctypes.POINTER(View),
@@ -129,6 +134,9 @@ _SIGNATURES = {
     "sgk_trisolve_grouped": (c_i32, [ctypes.POINTER(TriGroups), ctypes.POINTER(TriGroups),
                                      ctypes.POINTER(SegView), ctypes.POINTER(SegView), c_vp, c_i32, c_i32,
                                      c_vp]),
+    "sgk_fastdiag_work_doubles": (c_i64, [ctypes.POINTER(FastDiag), c_i32]),
+    "sgk_fastdiag_solve": (c_i32, [ctypes.POINTER(FastDiag), ctypes.POINTER(SegView), ctypes.POINTER(SegView),
+                                   c_vp, c_i32, c_vp]),
     "sgk_cheb_step": (c_i32, [ctypes.POINTER(Pattern), c_i32, c_vp, c_i64, c_vp, c_vp, c_vp,
                               c_vp, c_dbl, c_vp]),
     "sgk_colscale": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_i32, c_dbl, c_vp, c_vp]),

@@ -1,0 +1,143 @@
+// Depth-free lead solves by fast diagonalisation.
+//
+// On a tensor grid with a constant-coefficient lead the reference's sparse
+// LU (linalg.py:103-120) factors a Kronecker sum:
+//   A = K1 (x) M1 + M1 (x) K1,   M = M1 (x) M1     (node p = iy*n + ix),
+// and with the generalised eigenpairs K1 S = M1 S diag(mu), S^T M1 S = I:
+//   (S (x) S)^T A (S (x) S) = diag(mu_a + mu_b),  (S (x) S)^T M (S (x) S) = I.
+// So A^-1 = T diag(1/lam) T^T and the hGSoc block
+//   P~ = [M 0 -A; 0 beta M M; -A M 0]   (preconditioners.py:437-448)
+// becomes one 3x3 system per mode:  P~^-1 = T' B(lam)^-1 T'^T with
+//   B^-1 = d [[1, lam, -beta lam], [lam, lam^2, 1], [-beta lam, 1, -beta]],
+//   d = 1 / (1 + beta lam^2).
+// A solve is four dense passes (S^T along ix, S^T along iy, S along iy, S
+// along ix) — plain fp64 GEMMs, run by cuBLAS — around one modal kernel.
+// No dependency chain: the cost is 24 n^3 flops per right-hand-side column
+// and segment instead of the factor's level depth.
+#include <cublas_v2.h>
+
+#include <mutex>
+
+#include "sgk_common.cuh"
+
+namespace sgk {
+
+static cublasHandle_t blas_handle() {
+  static cublasHandle_t h = nullptr;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) h = nullptr;
+  return h;
+}
+
+// t[p*width + k] *= 1/lam[p]   (p = a*n + b mode index)
+__global__ void fastdiag_modal1_kernel(double* __restrict__ t, const double* __restrict__ lam, int64_t n_modes,
+                                       int width) {
+  const int64_t total = n_modes * width;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    t[i] = t[i] / lam[(uint64_t)i / (uint32_t)width];
+  }
+}
+
+// the 3x3 modal solve of P~ on three segments (y, u, lambda) in place
+__global__ void fastdiag_modal3_kernel(double* __restrict__ t0, double* __restrict__ t1, double* __restrict__ t2,
+                                       const double* __restrict__ lam, double beta, int64_t n_modes, int width) {
+  const int64_t total = n_modes * width;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const double l = lam[(uint64_t)i / (uint32_t)width];
+    const double r1 = t0[i], r2 = t1[i], r3 = t2[i];
+    const double d = 1.0 / fma(beta * l, l, 1.0);
+    t0[i] = d * (r1 + l * (r2 - beta * r3));
+    t1[i] = d * (l * (r1 + l * r2) + r3);
+    t2[i] = d * (r2 - beta * (l * r1 + r3));
+  }
+}
+
+static int blas_check(cublasStatus_t st, const char* what) {
+  if (st != CUBLAS_STATUS_SUCCESS) {
+    set_error(std::string("sgk_fastdiag_solve: ") + what + " failed (cublas status " + std::to_string((int)st) + ")");
+    return SGK_ECUDA;
+  }
+  return SGK_OK;
+}
+
+}  // namespace sgk
+
+extern "C" int64_t sgk_fastdiag_work_doubles(const sgk_fastdiag* fd, int32_t width) {
+  if (!fd || fd->n <= 0 || width < 0) return -1;
+  return 2 * (int64_t)fd->n_seg * fd->n * fd->n * width;
+}
+
+extern "C" int sgk_fastdiag_solve(const sgk_fastdiag* fd, const sgk_segview* b, const sgk_segview* x, double* work,
+                                  int32_t width, void* stream) {
+  using namespace sgk;
+  SGK_REQUIRE(fd && b && x && fd->s && fd->st && fd->lam, "sgk_fastdiag_solve: null argument");
+  SGK_REQUIRE(fd->n > 0 && (fd->n_seg == 1 || fd->n_seg == 3), "sgk_fastdiag_solve: bad factor (n, n_seg)");
+  SGK_REQUIRE(width >= 0, "sgk_fastdiag_solve: negative width");
+  if (width == 0) return SGK_OK;
+  const int n = fd->n;
+  const int64_t n2 = (int64_t)n * n;
+  SGK_REQUIRE(b->seg_rows == n2 && x->seg_rows == n2, "sgk_fastdiag_solve: segment rows != n*n");
+  SGK_REQUIRE(b->ld >= b->col0 + width && x->ld >= x->col0 + width, "sgk_fastdiag_solve: view narrower than width");
+  SGK_REQUIRE(work != nullptr, "sgk_fastdiag_solve: null workspace");
+  for (int s = 0; s < fd->n_seg; ++s)
+    SGK_REQUIRE(b->ptr[s] && x->ptr[s], "sgk_fastdiag_solve: null segment");
+  cublasHandle_t h = blas_handle();
+  if (!h) {
+    set_error("sgk_fastdiag_solve: cublasCreate failed");
+    return SGK_ECUDA;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (int rc = blas_check(cublasSetStream(h, st), "cublasSetStream")) return rc;
+  cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST);
+  const double one = 1.0, zero = 0.0;
+  const int64_t seg = n2 * width;  // doubles per segment of one pass buffer
+  double* t1 = work;
+  double* t2 = work + fd->n_seg * seg;
+  const int nw = n * width;
+  // cuBLAS is column-major: a row-major (rows x width, ld) block is a
+  // column-major (width x rows, ld) matrix.  fd->st (row-major S^T) is S in
+  // column-major order, fd->s (row-major S) is S^T in column-major order.
+  for (int s = 0; s < fd->n_seg; ++s) {
+    // pass 1: T1[iy][b][k] = sum_ix S[ix,b] X[iy*n+ix][k]      (batch over iy)
+    if (int rc = blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, width, n, n, &one,
+                                                      b->ptr[s] + b->col0, (int)b->ld, (long long)n * b->ld, fd->st,
+                                                      n, 0, &zero, t1 + s * seg, width, (long long)nw, n),
+                            "pass 1"))
+      return rc;
+  }
+  // pass 2: T2[a][b][k] = sum_iy S[iy,a] T1[iy][b][k]            (batch over segments)
+  if (int rc = blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, nw, n, n, &one, t1, nw,
+                                                    (long long)seg, fd->st, n, 0, &zero, t2, nw, (long long)seg,
+                                                    fd->n_seg),
+                          "pass 2"))
+    return rc;
+  {
+    const int64_t total = n2 * width;
+    const int threads = 256;
+    int64_t blocks = (total + threads - 1) / threads;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    if (fd->n_seg == 1)
+      fastdiag_modal1_kernel<<<(int)blocks, threads, 0, st>>>(t2, fd->lam, n2, width);
+    else
+      fastdiag_modal3_kernel<<<(int)blocks, threads, 0, st>>>(t2, t2 + seg, t2 + 2 * seg, fd->lam, fd->beta, n2,
+                                                              width);
+    if (int rc = check_launch("fastdiag_modal_kernel")) return rc;
+  }
+  // pass 3: T1[iy][b][k] = sum_a S[iy,a] T2[a][b][k]
+  if (int rc = blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, nw, n, n, &one, t2, nw,
+                                                    (long long)seg, fd->s, n, 0, &zero, t1, nw, (long long)seg,
+                                                    fd->n_seg),
+                          "pass 3"))
+    return rc;
+  for (int s = 0; s < fd->n_seg; ++s) {
+    // pass 4: X[iy*n+ix][k] = sum_b S[ix,b] T1[iy][b][k]
+    if (int rc = blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, width, n, n, &one, t1 + s * seg,
+                                                      width, (long long)nw, fd->s, n, 0, &zero, x->ptr[s] + x->col0,
+                                                      (int)x->ld, (long long)n * x->ld, n),
+                            "pass 4"))
+      return rc;
+  }
+  return SGK_OK;  // only the modal kernel is counted in sgk_launch_count (the GEMMs are cuBLAS)
+}

@@ -30,6 +30,7 @@ from scipy.sparse import csr_matrix
 from . import _lib
 from .basis import LevelPartition
 from .device import DevicePattern, DeviceProgram, as_device_state, run_program
+from .fastdiag import fastdiag_factor, fastdiag_kkt_factor
 from .linalg import LUFactors, sparse_lu
 from .operators import KroneckerSumOperator, SteadyKKT, _finish, kron_apply
 from .program import compile_program, coupling_from_csr
@@ -40,6 +41,7 @@ __all__ = [
     "CHEB_LAMBDA_MIN",
     "ChebyshevConfig",
     "CoupledSweepPreconditioner",
+    "LEAD_SOLVERS",
     "HierarchicalGaussSeidel",
     "SteadyKKTPreconditioner",
     "build_coupled_preconditioner",
@@ -244,13 +246,31 @@ def shifted_lead_terms(sys: SteadyKKT) -> list[csr_matrix]:
     return [lead] + [a.tocsr() for a in sys.stiffness[1:]]
 
 
-def build_sweep(couplings, terms, partition: LevelPartition, n_tau: int):
+LEAD_SOLVERS = ("lu", "fastdiag")
+
+
+def _lead_factor(lead, mass, lead_solver: str):
+    """The lead-term factor: the reference's SuperLU ("lu", default; GPU
+    triangular solves) or the depth-free fast diagonalisation of a
+    Kronecker-sum lead ("fastdiag"; needs the mass
+    matrix, raises ValueError when the lead is not a Kronecker sum)."""
+    if lead_solver == "lu":
+        return sparse_lu(lead)
+    if lead_solver == "fastdiag":
+        if mass is None:
+            raise ValueError("lead_solver='fastdiag' needs the mass matrix")
+        return fastdiag_factor(lead, mass)
+    raise ValueError(f"unknown lead solver {lead_solver!r} (expected one of {LEAD_SOLVERS})")
+
+
+def build_sweep(couplings, terms, partition: LevelPartition, n_tau: int, *, lead_solver: str = "lu",
+                mass=None):
     """Kronecker operator + sweep with a host-factored lead term
     (reference :211-224).  With unshifted stiffness terms this is the hGS
     preconditioner of the forward problem (configs 1 and 3)."""
     op = KroneckerSumOperator(couplings=list(couplings), operators=list(terms))
     sweep = HierarchicalGaussSeidel(operator=op, partition=partition, n_tau=n_tau,
-                                    lead_factor=sparse_lu(terms[0]))
+                                    lead_factor=_lead_factor(terms[0], mass, lead_solver))
     return op, sweep
 
 
@@ -324,9 +344,11 @@ class SteadyKKTPreconditioner:
 
 
 def build_steady_preconditioner(sys: SteadyKKT, partition: LevelPartition, mass_solver: str = "cheb5",
-                                n_tau: int | None = None, richardson_steps: int = 1) -> SteadyKKTPreconditioner:
+                                n_tau: int | None = None, richardson_steps: int = 1, *,
+                                lead_solver: str = "lu") -> SteadyKKTPreconditioner:
     n_tau = sys.n_terms if n_tau is None else n_tau
-    z_op, sweep = build_sweep(sys.triple.matrices[: sys.n_terms], shifted_lead_terms(sys), partition, n_tau)
+    z_op, sweep = build_sweep(sys.triple.matrices[: sys.n_terms], shifted_lead_terms(sys), partition, n_tau,
+                              lead_solver=lead_solver, mass=sys.mass)
     if mass_solver.startswith("cheb"):
         ms = make_mass_solver(sys.mass, mass_solver, sys.pattern, sys.mass_slice)
     else:
@@ -420,9 +442,16 @@ def deterministic_kkt_matrix(sys: SteadyKKT) -> csr_matrix:
 
 
 def build_coupled_preconditioner(sys: SteadyKKT, partition: LevelPartition,
-                                 n_tau: int | None = None) -> CoupledSweepPreconditioner:
+                                 n_tau: int | None = None, *, lead_solver: str = "lu") -> CoupledSweepPreconditioner:
+    """hGSoc with the P~ factor from SuperLU ("lu", the reference's
+    preconditioners.py:451-462) or the fast diagonalisation ("fastdiag")."""
     n_tau = sys.n_terms if n_tau is None else n_tau
     if not 1 <= n_tau <= sys.n_terms:
         raise ValueError("n_tau out of range")
-    return CoupledSweepPreconditioner(system=sys, partition=partition, n_tau=n_tau,
-                                      kkt_factor=sparse_lu(deterministic_kkt_matrix(sys)))
+    if lead_solver == "lu":
+        factor = sparse_lu(deterministic_kkt_matrix(sys))
+    elif lead_solver == "fastdiag":
+        factor = fastdiag_kkt_factor(sys.stiffness[0], sys.mass, sys.beta)
+    else:
+        raise ValueError(f"unknown lead solver {lead_solver!r} (expected one of {LEAD_SOLVERS})")
+    return CoupledSweepPreconditioner(system=sys, partition=partition, n_tau=n_tau, kkt_factor=factor)

@@ -302,11 +302,15 @@ class TimeKKTPreconditioner:
 
 
 def build_time_preconditioner(sys: TimeKKT, partition: LevelPartition, mass_solver: str = "cheb5",
-                              n_tau: int | None = None, richardson_steps: int = 1) -> TimeKKTPreconditioner:
-    """Reference preconditioners.py:315-333."""
+                              n_tau: int | None = None, richardson_steps: int = 1, *,
+                              lead_solver: str = "lu") -> TimeKKTPreconditioner:
+    """Reference preconditioners.py:315-333 (lead_solver as in
+    preconditioners.build_sweep: "lu" = the reference's SuperLU, "fastdiag" =
+    the depth-free Kronecker-sum solve)."""
     st = sys.steady
     n_tau = st.n_terms if n_tau is None else n_tau
-    z_op, sweep = build_sweep(st.triple.matrices[: st.n_terms], time_lead_terms(sys), partition, n_tau)
+    z_op, sweep = build_sweep(st.triple.matrices[: st.n_terms], time_lead_terms(sys), partition, n_tau,
+                              lead_solver=lead_solver, mass=st.mass)
     if mass_solver.startswith("cheb"):
         ms = make_mass_solver(st.mass, mass_solver, st.pattern, st.mass_slice)
     else:
