@@ -522,6 +522,16 @@ def run_ours(args):
         if args.solve_time:
             solves["time_dependent"] = time_solve_block(args.time_cpu)
         line["solves"] = solves
+    if rank == 0 and args.table_out:
+        from paper_2512_23804_b200.problems import build_problem
+        from paper_2512_23804_b200.tables import emit_table, experiment_rows
+
+        rows = experiment_rows(build_problem(2), lead_solver=args.table_lead)
+        b5 = build_problem(5)
+        for beta in (1e-2, 1e-4, 1e-6):
+            rows += experiment_rows(b5, n_taus=[b5.n_terms], beta=beta, lead_solver=args.table_lead)
+        with open(args.table_out, "w") as fh:
+            fh.write(emit_table(rows, "markdown" if args.table_out.endswith(".md") else "csv"))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -541,6 +551,9 @@ def main():
     ap.add_argument("--solve-time", action="store_true", help="time-dependent PINT solve (SURVEY 8(f) row 1)")
     ap.add_argument("--time-cpu", action="store_true", help="also time the CPU port of the time-dependent solve")
     ap.add_argument("--ref-budget", type=float, default=3.0)
+    ap.add_argument("--table-out", default=None,
+                    help="also write the reference-schema result table (.csv or .md) of the cfg2/cfg5 experiment rows")
+    ap.add_argument("--table-lead", choices=["lu", "fastdiag"], default="lu")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -331,6 +331,14 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
     // the dynamic shared memory; the host orders every lane's entries so the
     // rows' U loads repeat few bank pairs per half-warp
     constexpr int IL = MAXOUT < SGK_S9_IL ? MAXOUT : SGK_S9_IL;
+    // single-output programs: this row's output / init rows resolved once
+    // (the per-column epilogue is then one multiply-add and one store)
+    double* orow = nullptr;
+    const double* irow = nullptr;
+    if constexpr (ONEOUT) {
+      orow = out.v[0].ptr + (int64_t)row * out.v[0].ld + out.v[0].col0;
+      if (init.v[0].ptr != nullptr) irow = init.v[0].ptr + (int64_t)row * init.v[0].ld + init.v[0].col0;
+    }
 #pragma unroll
     for (int rb = 0; rb < MAXOUT; rb += IL) {
       int cnt[IL], gofs[IL];
@@ -366,12 +374,18 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
         const int oc = ocol[rb + i];
         if (oc >= 0) {
           const double acc = acc0[i] + acc1[i];
-          const int o = ONEOUT ? 0 : oc >> 24, k = oc & 0xFFFFFF;
-          double y = pick_s(alpha, o) * acc;
-          const sgk_view& iv = pick(init, o);
-          if (iv.ptr != nullptr) y += pick_s(beta, o) * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
-          const sgk_view& ov = pick(out, o);
-          ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
+          if constexpr (ONEOUT) {
+            double y = alpha.s[0] * acc;
+            if (irow != nullptr) y = fma(beta.s[0], irow[oc], y);
+            orow[oc] = y;
+          } else {
+            const int o = oc >> 24, k = oc & 0xFFFFFF;
+            double y = pick_s(alpha, o) * acc;
+            const sgk_view& iv = pick(init, o);
+            if (iv.ptr != nullptr) y += pick_s(beta, o) * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
+            const sgk_view& ov = pick(out, o);
+            ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
+          }
         }
       }
     }

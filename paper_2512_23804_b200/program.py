@@ -675,17 +675,23 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
         rows = _assign_rows([lanes.get(ln, []) for ln in range(32)], zero_of_bank) if lanes else \
             np.zeros((0, 32), np.int64)
         blocks.append(rows.astype(np.uint32))
-    # chunk c is gathered by warp c % warps (the launcher's warp count): give
-    # each warp chunks of similar row counts
+    # chunk slot j is gathered by warp j % warps (the launcher's warp count):
+    # balance the warps' total gather rows (longest-processing-time first),
+    # since the barrier after the gather waits for the busiest warp
     n_groups = len(group_info) - 1
     warps = stencil9_warps(n_groups, n_chunks)
     per_warp = -(-n_chunks // warps) if n_chunks else 0
     n_slots = per_warp * warps
-    order = sorted(range(n_chunks), key=lambda c: -len(blocks[c]))
+    order = sorted(range(n_chunks), key=lambda c: (-len(blocks[c]), c))
     slot_of_chunk = {}
-    for j, c in enumerate(order):
-        w, r = j // per_warp, j % per_warp
-        slot_of_chunk[c] = w + r * warps
+    load = [0] * warps
+    used = [0] * warps
+    for c in order:
+        w = min((w for w in range(warps) if used[w] < per_warp), key=lambda w: (load[w], w))
+        slot_of_chunk[c] = w + used[w] * warps
+        used[w] += 1
+        load[w] += len(blocks[c])
+    stats_extra["gather_rows_max_warp"] = int(max(load)) if load else 0
     chunk_meta = [(0, 0)] * n_slots
     out_col = -np.ones(n_slots * 32, np.int64)
     ents, off = [], 0
