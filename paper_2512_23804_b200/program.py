@@ -596,11 +596,7 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
     # Product (s, l, t) lives at slot base + (lane0 ^ sw[q]), base = group base
     # + 128 qq + 32 c: a per-step XOR swizzle (< 16) keeps the producer's STS
     # conflict-free and spreads the gather over bank pairs.
-    group_info = []
-    step_rec = []
-    prod_of = {}  # (s, l, t) -> (q, base, lane0)
-    n_ubuf = 0
-    executed = 0
+    specs = []  # (s, col0, ncols, [(t, [l...]) ...])
     for s in np.unique(s_arr):
         sel = s_arr == s
         cols = np.unique(l_arr[sel])
@@ -617,17 +613,39 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
                 ncols = span_hi - col0
             in_g = (ls_s >= col0) & (ls_s < col0 + ncols)
             gt, gl = ts_s[in_g], ls_s[in_g] - col0
-            q0 = len(step_rec)
-            group_info.append((int(s), col0, ncols, q0))
-            for qq, t in enumerate(np.unique(gt)):
-                step_rec.append(int(t))
-                for l in np.unique(gl[gt == t]):
-                    key = (int(s), col0 + int(l), int(t))
-                    if key not in prod_of:
-                        prod_of[key] = (q0 + qq, n_ubuf + qq * GROUP_COLS + (int(l) // 32) * 32, int(l) % 32)
-                executed += GROUP_COLS
-            n_ubuf += GROUP_COLS * (len(step_rec) - q0)
+            specs.append((int(s), col0, ncols, [(int(t), np.unique(gl[gt == t])) for t in np.unique(gt)]))
             i = j
+    # group position g is run by warp g % warps when there are more groups
+    # than warps (8): place them longest-first on the least-loaded warp that
+    # still has a position, so the products phase ends together
+    n_warps_prod = 8
+    if len(specs) > n_warps_prod:
+        cap = [len(range(w, len(specs), n_warps_prod)) for w in range(n_warps_prod)]
+        load = [0] * n_warps_prod
+        used = [0] * n_warps_prod
+        pos = [0] * len(specs)
+        for gi in sorted(range(len(specs)), key=lambda g: (-len(specs[g][3]), g)):
+            w = min((w for w in range(n_warps_prod) if used[w] < cap[w]), key=lambda w: (load[w], w))
+            pos[gi] = w + used[w] * n_warps_prod
+            used[w] += 1
+            load[w] += len(specs[gi][3])
+        specs = [specs[g] for g in np.argsort(pos)]
+    group_info = []
+    step_rec = []
+    prod_of = {}  # (s, l, t) -> (q, base, lane0)
+    n_ubuf = 0
+    executed = 0
+    for s, col0, ncols, terms in specs:
+        q0 = len(step_rec)
+        group_info.append((s, col0, ncols, q0))
+        for qq, (t, ls) in enumerate(terms):
+            step_rec.append(t)
+            for l in ls:
+                key = (s, col0 + int(l), t)
+                if key not in prod_of:
+                    prod_of[key] = (q0 + qq, n_ubuf + qq * GROUP_COLS + (int(l) // 32) * 32, int(l) % 32)
+            executed += GROUP_COLS
+        n_ubuf += GROUP_COLS * (len(step_rec) - q0)
     n_steps = len(step_rec)
     if n_steps and max(step_rec) >= (1 << 16):
         return None
