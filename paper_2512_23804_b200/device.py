@@ -28,6 +28,9 @@ F64 = torch.float64
 import os as _os
 
 FAST9 = _os.environ.get("SGKKT_FAST9", "1") != "0"
+# output columns one launch can hold (16 gather chunks x 256 threads in both
+# kernels); wider programs are launched per column block
+MAX_LAUNCH_COLS = 16 * 256
 
 
 def device() -> torch.device:
@@ -223,11 +226,36 @@ class DeviceProgram:
             self._fast9[n_slices] = _Program9(host) if host is not None else None
         return self._fast9[n_slices]
 
+    def column_parts(self, max_cols: int):
+        """Single-output sub-programs covering <= max_cols output columns each
+        (one CTA holds at most MAX_LAUNCH_COLS output columns of a row): a list
+        of (output index, first column, sub-program)."""
+        key = ("parts", max_cols)
+        parts = self._fast9.get(key)
+        if parts is None:
+            from .program import Coupling
+
+            parts = []
+            for o, w in enumerate(self._widths):
+                for k0 in range(0, w, max_cols):
+                    k1 = min(w, k0 + max_cols)
+                    sub = []
+                    for c in self.couplings:
+                        if c.o != o:
+                            continue
+                        keep = (c.cols >= k0) & (c.cols < k1)
+                        if np.any(keep):
+                            sub.append(Coupling(s=c.s, o=0, t=c.t, rows=c.rows[keep], cols=c.cols[keep] - k0,
+                                                vals=c.vals[keep]))
+                    parts.append((o, k0, DeviceProgram(sub, (k1 - k0,), n_inputs=self.n_inputs)))
+            self._fast9[key] = parts
+        return parts
+
     @property
     def host(self):
         """Schedule statistics of the fast path compiled last (else the general one)."""
-        for f in self._fast9.values():
-            if f is not None:
+        for k, f in self._fast9.items():
+            if f is not None and not isinstance(k, tuple):
                 return f.host
         return self.generic.host
 
@@ -261,6 +289,16 @@ def run_program(
     for (t, c0), w in zip(outputs, program.out_widths):
         if t.shape[0] != pattern.n_rows or c0 + w > t.shape[1]:
             raise ValueError("output view does not fit the program")
+    if sum(program.out_widths) > MAX_LAUNCH_COLS:
+        # wider than one CTA's output columns: one launch per column block
+        inits_l = inits or [None] * n_out
+        for o, k0, sub in program.column_parts(MAX_LAUNCH_COLS):
+            t, c0 = outputs[o]
+            ini = inits_l[o]
+            run_program(pattern, sub, inputs, [(t, c0 + k0)], [(ini[0], ini[1] + k0) if ini is not None else None],
+                        alpha=[(alpha or [1.0] * n_out)[o]], beta=[(beta or [1.0] * n_out)[o]], threads=threads,
+                        stream=stream, rows=rows)
+        return
     for t, c0 in inputs:
         if t.shape[0] != pattern.n_cols:
             raise ValueError("input rows do not match the operator")
