@@ -76,9 +76,6 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 #ifndef SGK_S9_MINB
 #define SGK_S9_MINB 2
 #endif
-#ifndef SGK_S9_IL
-#define SGK_S9_IL 1  // gather chunks walked together (1 measured best: 1.47 vs 1.73 ms at 4)
-#endif
 template <int MAXOUT, bool RESIDENT, bool ONEOUT>
 __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
                                                           ViewSet out, ViewSet init, ScalarSet alpha,
@@ -325,12 +322,12 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
 
     __syncthreads();  // (B) all U of this row in ubuf
 
-    // gather: the warp's chunks (chunk = warp + r*nwarps) are walked
-    // together, IL at a time, so their entry rows are independent loads in
-    // flight; entry = (ubuf byte offset << 14) | ctab byte offset relative to
-    // the dynamic shared memory; the host orders every lane's entries so the
+    // gather: the warp's chunk slots (chunk = warp + r*nwarps); a chunk has
+    // an even number of entry rows (host-padded with zero entries) stored as
+    // per-lane pairs, so one 8-byte load fetches the entries of two rows;
+    // entry = (ubuf byte offset << 14) | ctab byte offset relative to the
+    // dynamic shared memory; the host orders every lane's entries so the
     // rows' U loads repeat few bank pairs per half-warp
-    constexpr int IL = MAXOUT < SGK_S9_IL ? MAXOUT : SGK_S9_IL;
     // single-output programs: this row's output / init rows resolved once
     // (the per-column epilogue is then one multiply-add and one store)
     double* orow = nullptr;
@@ -340,52 +337,34 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
       if (init.v[0].ptr != nullptr) irow = init.v[0].ptr + (int64_t)row * init.v[0].ld + init.v[0].col0;
     }
 #pragma unroll
-    for (int rb = 0; rb < MAXOUT; rb += IL) {
-      int cnt[IL], gofs[IL];
-      double acc0[IL], acc1[IL];
-      int emax = 0;
-#pragma unroll
-      for (int i = 0; i < IL; ++i) {
-        const int chunk = warp + (rb + i) * nwarps;
-        const bool ok = chunk < n_chunks;
-        cnt[i] = ok ? ccnt[chunk] : 0;
-        gofs[i] = (ok ? coff[chunk] : 0) + lane;
-        acc0[i] = 0.0;
-        acc1[i] = 0.0;
-        emax = max(emax, cnt[i]);
+    for (int rb = 0; rb < MAXOUT; ++rb) {
+      const int chunk = warp + rb * nwarps;
+      if (chunk >= n_chunks) break;
+      const int npair = ccnt[chunk] >> 1;
+      const uint2* gp = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 2
+      for (int e = 0; e < npair; ++e, gp += 32) {
+        const uint2 w = *gp;
+        acc0 = fma(*reinterpret_cast<const double*>(sm + (w.x & 0x3FFF)),
+                   *reinterpret_cast<const double*>(sm + (w.x >> 14)), acc0);
+        acc1 = fma(*reinterpret_cast<const double*>(sm + (w.y & 0x3FFF)),
+                   *reinterpret_cast<const double*>(sm + (w.y >> 14)), acc1);
       }
-      for (int e = 0; e < emax; e += 2) {
-#pragma unroll
-        for (int i = 0; i < IL; ++i) {
-          if (e < cnt[i]) {
-            const uint32_t w0 = gent[gofs[i] + 32 * e];
-            acc0[i] = fma(*reinterpret_cast<const double*>(sm + (w0 & 0x3FFF)),
-                          *reinterpret_cast<const double*>(sm + (w0 >> 14)), acc0[i]);
-          }
-          if (e + 1 < cnt[i]) {
-            const uint32_t w1 = gent[gofs[i] + 32 * e + 32];
-            acc1[i] = fma(*reinterpret_cast<const double*>(sm + (w1 & 0x3FFF)),
-                          *reinterpret_cast<const double*>(sm + (w1 >> 14)), acc1[i]);
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < IL; ++i) {
-        const int oc = ocol[rb + i];
-        if (oc >= 0) {
-          const double acc = acc0[i] + acc1[i];
-          if constexpr (ONEOUT) {
-            double y = alpha.s[0] * acc;
-            if (irow != nullptr) y = fma(beta.s[0], irow[oc], y);
-            orow[oc] = y;
-          } else {
-            const int o = oc >> 24, k = oc & 0xFFFFFF;
-            double y = pick_s(alpha, o) * acc;
-            const sgk_view& iv = pick(init, o);
-            if (iv.ptr != nullptr) y += pick_s(beta, o) * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
-            const sgk_view& ov = pick(out, o);
-            ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
-          }
+      const int oc = ocol[rb];
+      if (oc >= 0) {
+        const double acc = acc0 + acc1;
+        if constexpr (ONEOUT) {
+          double y = alpha.s[0] * acc;
+          if (irow != nullptr) y = fma(beta.s[0], irow[oc], y);
+          orow[oc] = y;
+        } else {
+          const int o = oc >> 24, k = oc & 0xFFFFFF;
+          double y = pick_s(alpha, o) * acc;
+          const sgk_view& iv = pick(init, o);
+          if (iv.ptr != nullptr) y += pick_s(beta, o) * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
+          const sgk_view& ov = pick(out, o);
+          ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
         }
       }
     }

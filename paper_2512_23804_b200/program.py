@@ -688,10 +688,13 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
         pos = int(pos_e[i])
         per.setdefault(pos >> 5, {}).setdefault(pos & 31, []).append((int(payload[i]), int(bank[i])))
     blocks = []
+    zero_word = zero_of_bank[min(zero_of_bank)]
     for ch in range(n_chunks):
         lanes = per.get(ch)
         rows = _assign_rows([lanes.get(ln, []) for ln in range(32)], zero_of_bank) if lanes else \
             np.zeros((0, 32), np.int64)
+        if len(rows) % 2:  # even row count: the kernel reads rows in pairs
+            rows = np.vstack([rows, np.full((1, 32), zero_word, np.int64)])
         blocks.append(rows.astype(np.uint32))
     # chunk slot j is gathered by warp j % warps (the launcher's warp count):
     # balance the warps' total gather rows (longest-processing-time first),
@@ -721,7 +724,9 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
             continue
         blk = blocks[c]
         chunk_meta[j] = (len(blk), off)
-        ents.append(blk.reshape(-1))
+        # row pairs interleaved per lane: word 2*(32*e + lane) + {0, 1} holds
+        # rows 2e and 2e+1 of the lane (one 8-byte load per pair)
+        ents.append(blk.reshape(-1, 2, 32).transpose(0, 2, 1).reshape(-1))
         off += blk.size
         cols = col_at_pos[32 * c: 32 * c + 32]
         safe = np.maximum(cols, 0)
@@ -785,7 +790,7 @@ def emulate9(prog: HostProgram9, mats, inputs, inits, alpha, beta):
         cnt, off = int(meta[ch, 0]), int(meta[ch, 1])
         for e in range(cnt):
             for lane in range(32):
-                w = int(prog.gather_ent[off + e * 32 + lane])
+                w = int(prog.gather_ent[off + 2 * (32 * (e // 2) + lane) + e % 2])
                 acc[:, ch * 32 + lane] += prog.coef_tab[(w & 0x3FFF) // 8] * ub[:, ((w >> 14) - ubase) // 8]
     outs = [np.zeros((n_rows, w)) for w in prog.out_widths]
     for pos in range(n_chunks * 32):
