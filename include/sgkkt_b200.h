@@ -22,6 +22,8 @@
  *                          (preconditioners.py:155-164, 422-433)
  *   sgk_fastdiag_solve     linalg.py:76-87      LUFactors.solve for a Kronecker-sum lead
  *                          (A_1, A_1 + c M, and the P~ block of preconditioners.py:437-448)
+ *   sgk_q1_assemble        fem.py:171-206       assemble_stiffness / assemble_mass (all slices at once)
+ *   sgk_lognormal_fields   random_field.py:130-151 lognormal gPC coefficient fields
  *   sgk_cheb_step          preconditioners.py:70-98  chebyshev_mass_solve (one step)
  *   sgk_colscale           preconditioners.py:248-255 (column weights h^gamma, 1/beta)
  *   sgk_dot_partial,
@@ -254,6 +256,26 @@ int64_t sgk_fastdiag_work_doubles(const sgk_fastdiag* fd, int32_t width);
 int sgk_fastdiag_solve(const sgk_fastdiag* fd, const sgk_segview* b,
                        const sgk_segview* x, double* work, int32_t width,
                        void* stream);
+
+/* GPU setup pipeline.
+ * sgk_q1_assemble: the Q1 stiffness matrices of n_fields coefficient fields
+ * (fields: n_fields x n_elements x 4 Gauss-point samples, x fastest) and,
+ * with with_mass, the mass matrix as the last slice, assembled on the
+ * uniform n_cells^2 grid with boundary elimination (fem.py:171-206) into
+ * the pattern's t-stacked values (rowptr: the shared 9-point structure) and
+ * the padded 9-point layout (coef10: rows x S x 10, colind9: rows x 9; both
+ * may be NULL).  stiff_q: 4x4x4 reference gradient products per Gauss point
+ * [q][a][b]; mass_ref: 4x4, scaled by mass_weight.  Host pointers for
+ * stiff_q / mass_ref, device pointers for the rest.
+ * sgk_lognormal_fields: out[t][p] = mean[p] * prod_v g[v][p]^idx[t][v] /
+ * sqrt(idx[t][v]!)  (random_field.py:130-151).                              */
+int sgk_q1_assemble(int32_t n_cells, int32_t n_fields, const double* fields,
+                    const double* stiff_q, int32_t with_mass, double mass_weight,
+                    const double* mass_ref, const int32_t* rowptr, double* vals,
+                    double* coef10, int32_t* colind9, void* stream);
+int sgk_lognormal_fields(int64_t n_points, int32_t m, int32_t n_terms,
+                         const double* mean, const double* g, const int32_t* idx,
+                         double* out, void* stream);
 
 /* One Chebyshev semi-iteration step on all columns (preconditioners.py:89-97):
  * x_new = omega*(scale .* (b - M x) + x - x_prev) + x_prev,

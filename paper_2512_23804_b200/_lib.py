@@ -137,6 +137,8 @@ _SIGNATURES = {
     "sgk_fastdiag_work_doubles": (c_i64, [ctypes.POINTER(FastDiag), c_i32]),
     "sgk_fastdiag_solve": (c_i32, [ctypes.POINTER(FastDiag), ctypes.POINTER(SegView), ctypes.POINTER(SegView),
                                    c_vp, c_i32, c_vp]),
+    "sgk_q1_assemble": (c_i32, [c_i32, c_i32, c_vp, c_vp, c_i32, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "sgk_lognormal_fields": (c_i32, [c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "sgk_cheb_step": (c_i32, [ctypes.POINTER(Pattern), c_i32, c_vp, c_i64, c_vp, c_vp, c_vp,
                               c_vp, c_dbl, c_vp]),
     "sgk_colscale": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_i32, c_dbl, c_vp, c_vp]),

@@ -128,6 +128,69 @@ class DevicePattern:
             vals=self._vals.data_ptr(),
         )
 
+    @classmethod
+    def assemble_q1(cls, grid, fields, with_mass: bool = True) -> "DevicePattern":
+        """Device-assembled pattern: slices = the Q1
+        stiffness matrices of the coefficient fields (+ the mass matrix as
+        the last slice), built by csrc/assemble.cu directly into both device
+        layouts.  `fields` is a (T, n_elements, 4) float64 array or CUDA
+        tensor of Gauss-point samples (reference fem.py:171-206)."""
+        from . import fem
+
+        f = fields if isinstance(fields, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(fields, np.float64))
+        f = f.to(device(), dtype=F64).contiguous()
+        if f.dim() != 3 or f.shape[1] != grid.n_elements or f.shape[2] != 4:
+            raise ValueError("fields must have shape (T, n_elements, 4)")
+        T = int(f.shape[0])
+        S = T + (1 if with_mass else 0)
+        if S == 0:
+            raise ValueError("nothing to assemble")
+        struct_m = fem.assemble_mass(grid)  # the shared 9-point structure
+        self = cls.__new__(cls)
+        n = struct_m.shape[0]
+        self.n_rows = self.n_cols = n
+        self.n_slices = S
+        self.nnz = int(struct_m.nnz)
+        self.indptr = struct_m.indptr.astype(np.int64)
+        self.indices = struct_m.indices.astype(np.int64)
+        self._slice_data = None
+        lens = np.diff(self.indptr)
+        self.max_row_nnz = int(lens.max()) if n else 0
+        self._rowptr = _i32(self.indptr)
+        self._colind = _i32(self.indices)
+        self._vals = torch.empty(max(self.nnz * S, 1), dtype=F64, device=device())
+        self._colind9 = torch.empty((n, 9), dtype=torch.int32, device=device())
+        self._coef10 = torch.empty((n, S, 10), dtype=F64, device=device())
+        stiff_q = np.ascontiguousarray(fem._STIFF_Q, np.float64)
+        mass_ref = np.ascontiguousarray(fem._MASS_REF, np.float64)
+        rc = _lib.lib().sgk_q1_assemble(
+            grid.n_cells, T, f.data_ptr() if T else None, stiff_q.ctypes.data, int(with_mass),
+            float(grid.quad_weight), mass_ref.ctypes.data, self._rowptr.data_ptr(), self._vals.data_ptr(),
+            self._coef10.data_ptr(), self._colind9.data_ptr(), _lib.stream_ptr())
+        _lib.check(rc, "sgk_q1_assemble")
+        self.struct = _lib.Pattern(n_rows=n, n_slices=S, max_row_nnz=self.max_row_nnz, pad=0,
+                                   rowptr=self._rowptr.data_ptr(), colind=self._colind.data_ptr(),
+                                   vals=self._vals.data_ptr())
+        self._p9 = _lib.Pattern9(n_rows=n, n_slices=S, colind9=self._colind9.data_ptr(),
+                                 coef10=self._coef10.data_ptr())
+        return self
+
+    @property
+    def slice_data(self) -> np.ndarray:
+        """(T, nnz) slice values in CSR order (host copy; fetched from the
+        device for device-assembled patterns)."""
+        if self._slice_data is None:
+            lens = np.diff(self.indptr)
+            row_of = np.repeat(np.arange(self.n_rows), lens)
+            jj = np.arange(self.nnz) - self.indptr[row_of]
+            src = (self.indptr[row_of] * self.n_slices)[None, :] + np.arange(self.n_slices)[:, None] * lens[row_of][None, :] + jj[None, :]
+            self._slice_data = self._vals.cpu().numpy()[src]
+        return self._slice_data
+
+    @slice_data.setter
+    def slice_data(self, v):
+        self._slice_data = v
+
     def pattern9(self):
         """Padded 9-entry layout for the fast path (None if a row is longer)."""
         if self.max_row_nnz > 9:

@@ -126,7 +126,9 @@ class KroneckerSumOperator:
     def pattern(self) -> DevicePattern:
         pat = self._cache.get("pattern")
         if pat is None:
-            pat = DevicePattern(list(self.operators))
+            from .gpu_setup import attached_pattern
+
+            pat = attached_pattern(self.operators) or DevicePattern(list(self.operators))
             self._cache["pattern"] = pat
         return pat
 
@@ -306,7 +308,10 @@ class SteadyKKT:
         """Slices [A_0 .. A_{T-1}, M] on one pattern (M is slice T)."""
         pat = self._cache.get("pattern")
         if pat is None:
-            pat = DevicePattern(list(self.stiffness) + [self.mass])
+            from .gpu_setup import attached_pattern
+
+            mats = list(self.stiffness) + [self.mass]
+            pat = attached_pattern(mats) or DevicePattern(mats)
             self._cache["pattern"] = pat
         return pat
 
