@@ -354,23 +354,25 @@ def time_solve_block(with_cpu: bool):
     b = build_problem(spec, kl_method="dense")
     st = steady_system(b)
     sys_ = TimeKKT(steady=st, stencil=build_time_stencil(8), initial_state=np.zeros((st.n_h, st.n_xi)))
-    t0 = time.perf_counter()
-    prec = build_time_preconditioner(sys_, b.partition, "cheb5")
     rhs = time_rhs(sys_)
     bd = to_device_layout(sys_, rhs)
-    prec.apply(bd)
-    torch.cuda.synchronize()
-    t_setup = time.perf_counter() - t0
-    times = []
-    for _ in range(2):
-        torch.cuda.synchronize()
+    out = {"dofs": 3 * sys_.block_size(), "n_t": 8, "n_xi": st.n_xi, "n_terms": st.n_terms}
+    for ls in ("lu", "fastdiag"):
         t0 = time.perf_counter()
-        x, rep = fgmres(lambda v: time_kkt_apply(sys_, v), lambda v: prec.apply(v), bd, FgmresConfig(tol=1e-6))
+        prec = build_time_preconditioner(sys_, b.partition, "cheb5", lead_solver=ls)
+        prec.apply(bd)
         torch.cuda.synchronize()
-        times.append(time.perf_counter() - t0)
-    out = {"dofs": 3 * sys_.block_size(), "n_t": 8, "n_xi": st.n_xi, "n_terms": st.n_terms,
-           "gpu": {"iterations": rep.iterations, "converged": bool(rep.converged), "seconds": times[1],
-                   "first_solve_seconds": times[0], "setup_seconds": t_setup}}
+        t_setup = time.perf_counter() - t0
+        times = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            x, rep = fgmres(lambda v: time_kkt_apply(sys_, v), lambda v: prec.apply(v), bd, FgmresConfig(tol=1e-6))
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        out["gpu" if ls == "lu" else f"gpu[{ls}]"] = {
+            "iterations": rep.iterations, "converged": bool(rep.converged), "seconds": times[1],
+            "first_solve_seconds": times[0], "setup_seconds": t_setup}
     if with_cpu:
         import oracle
 

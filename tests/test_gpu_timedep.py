@@ -67,3 +67,28 @@ def test_pint_fgmres_solve_matches_reference():
     assert rep.converged and abs(rep.iterations - int(c["fgmres_iters"])) <= 1
     xf = from_device_layout(sys_, x)
     assert np.linalg.norm(xf - c["fgmres_x"]) <= 1e-8 * np.linalg.norm(c["fgmres_x"])
+
+
+def test_pint_with_fastdiag_leads_matches_reference():
+    """The time-shifted lead (1 + tau sqrt((1+gamma)/beta)) M + tau A_1 is a
+    Kronecker sum on the reference's tensor grid: the PINT preconditioner with
+    the depth-free lead solves reproduces the
+    reference's golden output to the fast diagonalisation's rounding and the
+    same FGMRES iteration count."""
+    import torch
+
+    from paper_2512_23804_b200.fastdiag import FastDiagFactors
+    from paper_2512_23804_b200.krylov import FgmresConfig, fgmres
+    from paper_2512_23804_b200.timedep import (build_time_preconditioner, from_device_layout, time_kkt_apply,
+                                               to_device_layout)
+
+    c, sys_, part = _system()
+    n_tau = int(c["n_terms"])
+    prec = build_time_preconditioner(sys_, part, mass_solver="cheb5", n_tau=n_tau, lead_solver="fastdiag")
+    assert isinstance(prec.sweep.lead_factor, FastDiagFactors)
+    assert _rel(prec.apply(c["v"]), c[f"pint_tau{n_tau}"]) <= 1e-11
+    b = to_device_layout(sys_, c["rhs"])
+    x, rep = fgmres(lambda v: time_kkt_apply(sys_, v), lambda v: prec.apply(v), b, FgmresConfig(tol=1e-6))
+    assert rep.converged and abs(rep.iterations - int(c["fgmres_iters"])) <= 1
+    xf = from_device_layout(sys_, x)
+    assert np.linalg.norm(xf - c["fgmres_x"]) <= 1e-8 * np.linalg.norm(c["fgmres_x"])
