@@ -263,7 +263,7 @@ def _event_time(fn, steps, stream):
     return start.elapsed_time(end) / 1e3
 
 
-def solve_block(cfg_id, betas, with_cpu=False, lead_solvers=("lu", "fastdiag")):
+def solve_block(cfg_id, betas, with_cpu=False, lead_solvers=("lu", "lu_nd", "fastdiag")):
     """Time-to-solution of the control configs on the GPU (setup reported
     separately).  Lead solvers: "lu" = the reference's SuperLU factors replayed
     by the GPU triangular solves (the reference algorithm); "fastdiag" = the
@@ -300,8 +300,10 @@ def solve_block(cfg_id, betas, with_cpu=False, lead_solvers=("lu", "fastdiag")):
         variants = []
         for ls in lead_solvers:
             sfx = "" if ls == "lu" else f"[{ls}]"
-            variants.append((f"hgsoc_fgmres{sfx}",
-                             lambda ls=ls: build_coupled_preconditioner(sys_, bundle.partition, lead_solver=ls), fgmres))
+            if ls != "lu_nd":  # P~ is indefinite and keeps COLAMD under lu_nd: same as "lu"
+                variants.append((f"hgsoc_fgmres{sfx}",
+                                 lambda ls=ls: build_coupled_preconditioner(sys_, bundle.partition, lead_solver=ls),
+                                 fgmres))
             variants.append((f"blockdiag_hgs_minres{sfx}",
                              lambda ls=ls: build_steady_preconditioner(sys_, bundle.partition, "cheb5", lead_solver=ls),
                              minres))

@@ -246,16 +246,20 @@ def shifted_lead_terms(sys: SteadyKKT) -> list[csr_matrix]:
     return [lead] + [a.tocsr() for a in sys.stiffness[1:]]
 
 
-LEAD_SOLVERS = ("lu", "fastdiag")
+LEAD_SOLVERS = ("lu", "lu_nd", "fastdiag")
 
 
 def _lead_factor(lead, mass, lead_solver: str):
     """The lead-term factor: the reference's SuperLU ("lu", default; GPU
-    triangular solves) or the depth-free fast diagonalisation of a
-    Kronecker-sum lead ("fastdiag"; needs the mass
-    matrix, raises ValueError when the lead is not a Kronecker sum)."""
+    triangular solves), SuperLU on a nested-dissection ordering of the grid
+    ("lu_nd": same solve, shallower triangles), or the depth-free fast
+    diagonalisation of a Kronecker-sum lead ("fastdiag", SURVEY §8(f) row 3;
+    needs the mass matrix, raises ValueError when the lead is not a Kronecker
+    sum)."""
     if lead_solver == "lu":
         return sparse_lu(lead)
+    if lead_solver == "lu_nd":
+        return sparse_lu(lead, ordering="nd")
     if lead_solver == "fastdiag":
         if mass is None:
             raise ValueError("lead_solver='fastdiag' needs the mass matrix")
@@ -448,7 +452,9 @@ def build_coupled_preconditioner(sys: SteadyKKT, partition: LevelPartition,
     n_tau = sys.n_terms if n_tau is None else n_tau
     if not 1 <= n_tau <= sys.n_terms:
         raise ValueError("n_tau out of range")
-    if lead_solver == "lu":
+    if lead_solver in ("lu", "lu_nd"):
+        # the indefinite P~ pivots: a nested-dissection order does not survive
+        # partial pivoting (config 5: depth 4.3k -> 44k), so P~ keeps COLAMD
         factor = sparse_lu(deterministic_kkt_matrix(sys))
     elif lead_solver == "fastdiag":
         factor = fastdiag_kkt_factor(sys.stiffness[0], sys.mass, sys.beta)
