@@ -339,6 +339,54 @@ def solve_block(cfg_id, betas, with_cpu=False, lead_solvers=("lu", "lu_nd", "fas
     return out
 
 
+def apply_breakdown(cfg_id, beta=1e-2):
+    """one KKT matvec (GB/s vs the HBM floor) and one hGSoc apply
+    split into its coupling launches and P~ solves, LU and fastdiag leads
+    (CUDA events, warm, 5 repetitions each)."""
+    import torch
+
+    from paper_2512_23804_b200.device import run_program
+    from paper_2512_23804_b200.operators import steady_kkt_apply_device
+    from paper_2512_23804_b200.preconditioners import build_coupled_preconditioner
+    from paper_2512_23804_b200.problems import build_problem, steady_system
+
+    stream = torch.cuda.current_stream()
+
+    def ms(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        return _event_time(fn, reps, stream) / reps * 1e3
+
+    b = build_problem(cfg_id)
+    s = steady_system(b, beta=beta)
+    shape = (s.n_h, s.n_xi)
+    rng = np.random.default_rng(SEED)
+    blocks = [torch.as_tensor(rng.standard_normal(shape)).cuda() for _ in range(3)]
+    outs = tuple(torch.empty_like(blocks[0]) for _ in range(3))
+    t_kkt = ms(lambda: steady_kkt_apply_device(s, *blocks, outs))
+    peak, _ = _peaks()
+    out = {"beta": beta, "kkt_matvec_ms": t_kkt, "kkt_algorithmic_bytes": s.algorithmic_bytes(),
+           "kkt_gbs": s.algorithmic_bytes() / (t_kkt * 1e-3) / 1e9}
+    out["kkt_hbm_frac"] = out["kkt_gbs"] / peak
+    for ls in ("lu", "fastdiag"):
+        soc = build_coupled_preconditioner(s, b.partition, lead_solver=ls)
+        fac = soc.kkt_factor.device_factors
+        fwd, bwd = soc._programs()
+        ranges = b.partition.ranges()
+        levels = list(zip(ranges, fwd)) + list(zip(reversed(ranges[:-1]), bwd))
+        rec = {"apply_ms": ms(lambda: soc.apply_device(*blocks, outs=outs)), "levels": []}
+        for (lo, hi), prog in levels:
+            segs = [(o, lo) for o in outs]
+            tc = ms(lambda: run_program(s.pattern, prog, [(o, 0) for o in outs], segs, [(r, lo) for r in blocks],
+                                        alpha=[1.0] * 3, beta=[1.0] * 3))
+            ts = ms(lambda: fac.solve_segments(segs, segs, hi - lo))
+            rec["levels"].append({"width": hi - lo, "coupling_ms": tc, "solve_ms": ts})
+        rec["couplings_ms"] = sum(lv["coupling_ms"] for lv in rec["levels"])
+        rec["solves_ms"] = sum(lv["solve_ms"] for lv in rec["levels"])
+        out[f"hgsoc_{ls}"] = rec
+    return out
+
+
 def time_solve_block(with_cpu: bool):
     """all-at-once time-dependent KKT with the PINT
     preconditioner inside the reference FGMRES (tol 1e-6, Chebyshev-5, hGS
@@ -448,6 +496,16 @@ def run_ours(args):
         dist.barrier()
     value = whole_job_gbs(B, args.steps, ws, t)
     kernel_avg = t / args.steps
+    # per-matvec distribution (median and best), separate pass
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for i in range(args.steps):
+        step()
+        evs[i + 1].record(stream)
+    evs[-1].synchronize()
+    per = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])
+    per_step = {"median_ms": float(np.median(per)), "best_ms": float(per.min()), "worst_ms": float(per.max()),
+                "median_gbs": B / (float(np.median(per)) * 1e-3) / 1e9, "best_gbs": B / (float(per.min()) * 1e-3) / 1e9}
 
     # e2e through the public API with pinned host buffers
     xp = torch.from_numpy(x_host).pin_memory()
@@ -508,6 +566,7 @@ def run_ours(args):
     }
     prog_stats = prog.host.stats
     line["config"]["schedule"] = prog_stats
+    line["per_step"] = per_step
     # fp64 work actually issued per launch (the kernel is DFMA-heavy: SURVEY §7 H1)
     useful = 2 * bundle.stiffness[0].nnz * prog_stats["n_products"] + 2 * bundle.n_h * prog_stats["n_gather"]
     line["roofline"]["fp64_flops_per_launch"] = useful
@@ -523,6 +582,7 @@ def run_ours(args):
         solves = {"cfg2": solve_block(2, [1e-2])}
         if not args.no_solve_cfg5:
             solves["cfg5"] = solve_block(5, [1e-2, 1e-4, 1e-6])
+            solves["cfg5_apply_breakdown"] = apply_breakdown(5)
         if args.solve_time:
             solves["time_dependent"] = time_solve_block(args.time_cpu)
         line["solves"] = solves
