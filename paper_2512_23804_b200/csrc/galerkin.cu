@@ -27,17 +27,22 @@
 namespace sgk {
 
 constexpr int kChunk = 9;          // stencil entries held in registers per pass
-constexpr int kStageMax = 2048;    // doubles of row coefficients staged in shared memory
+// the row's t-stacked coefficients are staged in shared memory when they fit
+// next to the U slots (many-term programs: config 3 has 924 slices x 9
+// entries = 66.5 KB per row; read from global memory they are 9 scattered
+// loads per product)
+constexpr size_t kSmemBudget = 200 * 1024;
 
 // STAGED: the row's t-stacked coefficients (n_slices*len doubles) are copied
-// to shared memory once per row and read back as warp broadcasts.
+// to shared memory once per row and read back from there (broadcasts when the
+// warp's lanes evaluate the same term).
 template <int MAXOUT, bool STAGED>
 __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_program prog,
                                                       ViewSet in, ViewSet out, ViewSet init,
-                                                      ScalarSet alpha, ScalarSet beta) {
+                                                      ScalarSet alpha, ScalarSet beta, int stage_n) {
   extern __shared__ double smem[];
-  double* coef_s = smem;                          // [kStageMax] when STAGED
-  double* ubuf = smem + (STAGED ? kStageMax : 0);  // U slots of one phase
+  double* coef_s = smem;                          // [stage_n] when STAGED
+  double* ubuf = smem + (STAGED ? stage_n : 0);    // U slots of one phase
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -50,6 +55,7 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
     const int32_t* crow = pat.colind + rs;
     if (STAGED) {
       const int nco = n_slices * len;
+      __syncthreads();  // the previous row's products are done with coef_s
       for (int i = threadIdx.x; i < nco; i += blockDim.x) coef_s[i] = __ldg(arow + i);
       __syncthreads();
     }
@@ -122,18 +128,58 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
       }
       __syncthreads();
       const int32_t* gp = prog.gather_ptr + (int64_t)p * prog.n_out_cols;
-#pragma unroll
-      for (int r = 0; r < MAXOUT; ++r) {
-        const int c = threadIdx.x + r * blockDim.x;
+      if constexpr (MAXOUT == 1) {
+        // fewer output columns than threads: `parts` threads share a column,
+        // thread part r takes entries r, r+parts, ... (coalesced table loads),
+        // four independent accumulation chains per thread
+        const int parts = max(1, (int)blockDim.x / max(prog.n_out_cols, 1));
+        const int c = threadIdx.x / parts, r = threadIdx.x - c * parts;
         if (c < prog.n_out_cols) {
           const int e0 = __ldg(gp + c), e1 = __ldg(gp + c + 1);
-          double a = acc[r];
-          for (int e = e0; e < e1; ++e)
-            a = fma(__ldg(prog.gather_coef + e), ubuf[__ldg(prog.gather_slot + e)], a);
-          acc[r] = a;
+          double a0 = acc[0], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int e = e0 + r;
+          for (; e + 3 * parts < e1; e += 4 * parts) {
+            const int s0 = __ldg(prog.gather_slot + e), s1 = __ldg(prog.gather_slot + e + parts);
+            const int s2 = __ldg(prog.gather_slot + e + 2 * parts), s3 = __ldg(prog.gather_slot + e + 3 * parts);
+            const double h0 = __ldg(prog.gather_coef + e), h1 = __ldg(prog.gather_coef + e + parts);
+            const double h2 = __ldg(prog.gather_coef + e + 2 * parts), h3 = __ldg(prog.gather_coef + e + 3 * parts);
+            a0 = fma(h0, ubuf[s0], a0);
+            a1 = fma(h1, ubuf[s1], a1);
+            a2 = fma(h2, ubuf[s2], a2);
+            a3 = fma(h3, ubuf[s3], a3);
+          }
+          for (; e < e1; e += parts) a0 = fma(__ldg(prog.gather_coef + e), ubuf[__ldg(prog.gather_slot + e)], a0);
+          acc[0] = (a0 + a1) + (a2 + a3);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < MAXOUT; ++r) {
+          const int c = threadIdx.x + r * blockDim.x;
+          if (c < prog.n_out_cols) {
+            const int e0 = __ldg(gp + c), e1 = __ldg(gp + c + 1);
+            double a = acc[r];
+            for (int e = e0; e < e1; ++e)
+              a = fma(__ldg(prog.gather_coef + e), ubuf[__ldg(prog.gather_slot + e)], a);
+            acc[r] = a;
+          }
         }
       }
       __syncthreads();
+    }
+    if constexpr (MAXOUT == 1) {
+      // combine the parts of each column in a fixed order (deterministic)
+      const int parts = max(1, (int)blockDim.x / max(prog.n_out_cols, 1));
+      if (parts > 1) {
+        ubuf[threadIdx.x] = acc[0];
+        __syncthreads();
+        const int c = threadIdx.x;
+        if (c < prog.n_out_cols) {
+          double a = ubuf[c * parts];
+          for (int r = 1; r < parts; ++r) a += ubuf[c * parts + r];
+          acc[0] = a;
+        }
+        __syncthreads();
+      }
     }
 
 #pragma unroll
@@ -149,15 +195,17 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
         ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
       }
     }
-    if (STAGED && prog.n_phases == 0) __syncthreads();  // coef_s reuse guard
   }
 }
 
 template <int MAXOUT, bool STAGED>
 static int launch_program_t(const sgk_pattern& pat, const sgk_program& prog, const ViewSet& in,
                             const ViewSet& out, const ViewSet& init, const ScalarSet& alpha,
-                            const ScalarSet& beta, int threads, cudaStream_t st) {
-  const size_t smem = (size_t)(prog.max_phase_slots + (STAGED ? kStageMax : 0)) * sizeof(double);
+                            const ScalarSet& beta, int threads, cudaStream_t st, int stage_n) {
+  // U slots of a phase; at least one double per thread (the column-parts
+  // reduction of single-chunk programs reuses the slots)
+  const int slots = prog.max_phase_slots > threads ? prog.max_phase_slots : threads;
+  const size_t smem = (size_t)(slots + (STAGED ? stage_n : 0)) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(program_kernel<MAXOUT, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -174,7 +222,7 @@ static int launch_program_t(const sgk_pattern& pat, const sgk_program& prog, con
   int64_t grid = (int64_t)sm_count() * occ;
   if (grid > pat.n_rows) grid = pat.n_rows;
   if (grid < 1) return SGK_OK;
-  program_kernel<MAXOUT, STAGED><<<(int)grid, threads, smem, st>>>(pat, prog, in, out, init, alpha, beta);
+  program_kernel<MAXOUT, STAGED><<<(int)grid, threads, smem, st>>>(pat, prog, in, out, init, alpha, beta, stage_n);
   return check_launch("program_kernel");
 }
 
@@ -182,9 +230,10 @@ template <int MAXOUT>
 static int launch_program(const sgk_pattern& pat, const sgk_program& prog, const ViewSet& in,
                           const ViewSet& out, const ViewSet& init, const ScalarSet& alpha,
                           const ScalarSet& beta, int threads, cudaStream_t st, int max_row_nnz) {
-  if ((int64_t)pat.n_slices * max_row_nnz <= kStageMax)
-    return launch_program_t<MAXOUT, true>(pat, prog, in, out, init, alpha, beta, threads, st);
-  return launch_program_t<MAXOUT, false>(pat, prog, in, out, init, alpha, beta, threads, st);
+  const int64_t stage_n = (int64_t)pat.n_slices * max_row_nnz;
+  if ((size_t)(stage_n + prog.max_phase_slots + threads) * sizeof(double) <= kSmemBudget)
+    return launch_program_t<MAXOUT, true>(pat, prog, in, out, init, alpha, beta, threads, st, (int)stage_n);
+  return launch_program_t<MAXOUT, false>(pat, prog, in, out, init, alpha, beta, threads, st, 0);
 }
 
 }  // namespace sgk

@@ -27,6 +27,7 @@ from scipy.sparse import csr_matrix
 
 from .basis import TripleProductSet
 from .device import DevicePattern, DeviceProgram, as_device_state, device, run_program
+from . import device as _dev
 from .program import Coupling, compile_program, coupling_from_csr
 
 __all__ = [
@@ -224,7 +225,7 @@ def kron_apply(op: KroneckerSumOperator, x, out=None):
     Pinned host tensors in/out take the overlapped slab pipeline."""
     n_h, n_xi = op.shape
     if (isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and isinstance(out, torch.Tensor)
-            and not out.is_cuda and out.is_pinned() and op.pattern.pattern9() is not None
+            and not out.is_cuda and out.is_pinned() and _dev.FAST9 and op.pattern.pattern9() is not None
             and tuple(x.shape) == (n_h, n_xi) and tuple(out.shape) == (n_h, n_xi) and x.dtype == torch.float64):
         return _kron_apply_pipelined(op, x.contiguous(), out)
     xd, host = as_device_state(x, (n_h, n_xi))
