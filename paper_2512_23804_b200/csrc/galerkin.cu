@@ -56,7 +56,13 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
     if (STAGED) {
       const int nco = n_slices * len;
       __syncthreads();  // the previous row's products are done with coef_s
-      for (int i = threadIdx.x; i < nco; i += blockDim.x) coef_s[i] = __ldg(arow + i);
+      // asynchronous 8-byte copies: every load of the block in flight at once
+      // (a load -> store loop serialises one memory latency per iteration)
+      for (int i = threadIdx.x; i < nco; i += blockDim.x) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(coef_s + i);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(arow + i) : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
       __syncthreads();
     }
     const double* abase = STAGED ? coef_s : arow;
@@ -88,10 +94,18 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
           for (int jj = 0; jj < kChunk; ++jj)
             v[jj] = (vb != nullptr && jj < cl) ? __ldg(vb + (int64_t)__ldg(crow + c0 + jj) * ldv) : 0.0;
           int q = q0;
-          // two independent steps per iteration (ILP across stencil dots)
+          // two independent steps per iteration (ILP across stencil dots);
+          // the next pair's term indices are loaded one iteration ahead (the
+          // step table is an L2 read when the staged block fills the SM)
+          int ta_n = q + 1 < q1 ? __ldg(prog.step_term + q * 32 + lane) : 0;
+          int tb_n = q + 1 < q1 ? __ldg(prog.step_term + (q + 1) * 32 + lane) : 0;
           for (; q + 1 < q1; q += 2) {
-            const int ta = __ldg(prog.step_term + q * 32 + lane);
-            const int tb = __ldg(prog.step_term + (q + 1) * 32 + lane);
+            const int ta = ta_n;
+            const int tb = tb_n;
+            if (q + 3 < q1) {
+              ta_n = __ldg(prog.step_term + (q + 2) * 32 + lane);
+              tb_n = __ldg(prog.step_term + (q + 3) * 32 + lane);
+            }
             const double* aa = abase + max(ta, 0) * len + c0;
             const double* ab = abase + max(tb, 0) * len + c0;
             double ua0 = 0.0, ua1 = 0.0, ub0 = 0.0, ub1 = 0.0;
