@@ -76,8 +76,10 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 #ifndef SGK_S9_MINB
 #define SGK_S9_MINB 2
 #endif
-template <int MAXOUT, bool RESIDENT, bool ONEOUT>
-__global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
+// BIG: 9..16 column groups, one CTA of up to 16 warps per SM so every group
+// stays resident (V prefetched) instead of warps looping over two groups
+template <int MAXOUT, bool RESIDENT, bool ONEOUT, bool BIG>
+__global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stencil9_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
                                                           ViewSet out, ViewSet init, ScalarSet alpha,
                                                           ScalarSet beta) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(256, SGK_S9_MINB) stencil9_kernel(sgk_pattern9
   cp_async_wait1();
 }
 
-template <int MAXOUT, bool RESIDENT, bool ONEOUT>
+template <int MAXOUT, bool RESIDENT, bool ONEOUT, bool BIG>
 static int launch9r(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
                     const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int threads, cudaStream_t st) {
   const Smem9 L = smem9_layout(pat.n_slices, prog);
@@ -382,14 +384,14 @@ static int launch9r(const sgk_pattern9& pat, const sgk_program9& prog, const Vie
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, stencil9_kernel<MAXOUT, RESIDENT, ONEOUT>);
-    cudaFuncSetAttribute(stencil9_kernel<MAXOUT, RESIDENT, ONEOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncGetAttributes(&fa, stencil9_kernel<MAXOUT, RESIDENT, ONEOUT, BIG>);
+    cudaFuncSetAttribute(stencil9_kernel<MAXOUT, RESIDENT, ONEOUT, BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          optin - (int)fa.sharedSizeBytes);
     cudaGetLastError();  // an attribute failure must not poison the launch check
     attr_set = true;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_kernel<MAXOUT, RESIDENT, ONEOUT>, threads, L.total);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_kernel<MAXOUT, RESIDENT, ONEOUT, BIG>, threads, L.total);
   if (occ < 1) {
     set_error("stencil9_kernel: program does not fit in shared memory (" + std::to_string(L.total) + " B)");
     return SGK_ELIMIT;
@@ -397,7 +399,7 @@ static int launch9r(const sgk_pattern9& pat, const sgk_program9& prog, const Vie
   int64_t grid = (int64_t)sm_count() * occ;
   if (grid > pat.n_rows) grid = pat.n_rows;
   if (grid < 1) return SGK_OK;
-  stencil9_kernel<MAXOUT, RESIDENT, ONEOUT><<<(int)grid, threads, L.total, st>>>(pat, prog, in, out, init, a, b);
+  stencil9_kernel<MAXOUT, RESIDENT, ONEOUT, BIG><<<(int)grid, threads, L.total, st>>>(pat, prog, in, out, init, a, b);
   return check_launch("stencil9_kernel");
 }
 
@@ -406,11 +408,19 @@ static int launch9(const sgk_pattern9& pat, const sgk_program9& prog, const View
                    const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int n_out, int threads,
                    cudaStream_t st) {
   const bool res = prog.n_groups <= threads / 32;
+  if (threads > 256) {
+    if (!res) {
+      set_error("stencil9_kernel: more than 16 column groups need the 256-thread kernel");
+      return SGK_EINVAL;
+    }
+    return n_out == 1 ? launch9r<MAXOUT, true, true, true>(pat, prog, in, out, init, a, b, threads, st)
+                      : launch9r<MAXOUT, true, false, true>(pat, prog, in, out, init, a, b, threads, st);
+  }
   if (n_out == 1)
-    return res ? launch9r<MAXOUT, true, true>(pat, prog, in, out, init, a, b, threads, st)
-               : launch9r<MAXOUT, false, true>(pat, prog, in, out, init, a, b, threads, st);
-  return res ? launch9r<MAXOUT, true, false>(pat, prog, in, out, init, a, b, threads, st)
-             : launch9r<MAXOUT, false, false>(pat, prog, in, out, init, a, b, threads, st);
+    return res ? launch9r<MAXOUT, true, true, false>(pat, prog, in, out, init, a, b, threads, st)
+               : launch9r<MAXOUT, false, true, false>(pat, prog, in, out, init, a, b, threads, st);
+  return res ? launch9r<MAXOUT, true, false, false>(pat, prog, in, out, init, a, b, threads, st)
+             : launch9r<MAXOUT, false, false, false>(pat, prog, in, out, init, a, b, threads, st);
 }
 
 }  // namespace sgk
@@ -432,7 +442,7 @@ extern "C" int sgk_stencil9_apply(const sgk_pattern9* pat, const sgk_program9* p
   SGK_REQUIRE((int64_t)prog->n_coef * 8 <= (1 << 14), "sgk_stencil9_apply: too many distinct coefficients");
   SGK_REQUIRE(prog->n_slices == pat->n_slices, "sgk_stencil9_apply: program compiled for another slice count");
   const int threads = block_threads > 0 ? block_threads : 256;
-  SGK_REQUIRE(threads % 32 == 0 && threads <= 256, "sgk_stencil9_apply: block_threads must be a multiple of 32, <=256");
+  SGK_REQUIRE(threads % 32 == 0 && threads <= 512, "sgk_stencil9_apply: block_threads must be a multiple of 32, <=512");
   ViewSet vin{}, vout{}, vinit{};
   ScalarSet a{}, b{};
   for (int i = 0; i < n_in; ++i) vin.v[i] = in[i];

@@ -376,10 +376,19 @@ class HostProgram9:
 GROUP_COLS = 128  # 4 column slots x 32 lanes
 
 
+# up to 16 warps (one 512-thread CTA per SM) so programs with 9..16 column
+# groups keep every group resident; SGKKT_S9_BIG=0 caps CTAs at 8 warps
+S9_BIG = os.environ.get("SGKKT_S9_BIG", "1") != "0"
+
+
 def stencil9_warps(n_groups: int, n_chunks: int) -> int:
     """Warps per CTA for stencil9_kernel: one per column group (resident V
-    registers) and at most 16 gather chunks per warp, 8 at most."""
-    return min(8, max(1, n_groups, -(-n_chunks // 16)))
+    registers) and at most 16 gather chunks per warp; 8 at most, 16 for
+    programs with 9..16 groups."""
+    w = max(1, n_groups, -(-n_chunks // 16))
+    if S9_BIG and 8 < n_groups <= 16:
+        return min(16, w)
+    return min(8, w)
 # bank-layout local search budget per program (deterministic; off by default:
 # cfg4 matvec 1.725 ms with it vs 1.728 ms without, and it costs ~3 s/program)
 SEARCH_MOVES = int(os.environ.get("SGKKT_S9_SEARCH_MOVES", "0"))
@@ -618,7 +627,7 @@ def compile_program9(couplings: list[Coupling], out_widths, *, n_inputs: int | N
     # group position g is run by warp g % warps when there are more groups
     # than warps (8): place them longest-first on the least-loaded warp that
     # still has a position, so the products phase ends together
-    n_warps_prod = 8
+    n_warps_prod = 16 if (S9_BIG and len(specs) <= 16) else 8
     if len(specs) > n_warps_prod:
         cap = [len(range(w, len(specs), n_warps_prod)) for w in range(n_warps_prod)]
         load = [0] * n_warps_prod
