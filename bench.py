@@ -339,6 +339,56 @@ def solve_block(cfg_id, betas, with_cpu=False, lead_solvers=("lu", "lu_nd", "fas
     return out
 
 
+def forward_block(cfg_id, n_taus=None, lead_solvers=("lu", "fastdiag")):
+    """BASELINE configs 1 and 3 (forward problem -div(a grad u) = 1): one
+    Galerkin matvec (GB/s, kernel path) and hGS-CG to 1e-8 per truncation
+    n_tau and lead solver (setup separate)."""
+    import torch
+
+    from paper_2512_23804_b200.krylov import FgmresConfig, cg
+    from paper_2512_23804_b200.operators import KroneckerSumOperator, kron_apply
+    from paper_2512_23804_b200.preconditioners import build_sweep
+    from paper_2512_23804_b200.problems import build_problem
+
+    t0 = time.perf_counter()
+    b = build_problem(cfg_id)
+    t_asm = time.perf_counter() - t0
+    cp = b.triple.matrices[: b.n_terms]
+    shape = (b.n_h, b.n_xi)
+    op = KroneckerSumOperator(couplings=cp, operators=b.stiffness)
+    x = torch.as_tensor(np.random.default_rng(SEED).standard_normal(shape)).cuda()
+    stream = torch.cuda.current_stream()
+    kron_apply(op, x)
+    torch.cuda.synchronize()
+    t_mv = _event_time(lambda: kron_apply(op, x), 10, stream) / 10
+    out = {"n_h": b.n_h, "n_xi": b.n_xi, "n_t": b.n_terms, "assembly_seconds": t_asm,
+           "matvec_ms": t_mv * 1e3, "matvec_gbs": op.algorithmic_bytes() / t_mv / 1e9,
+           "matvec_kernel": op.program([(0, b.n_xi)], (0, b.n_xi), 0, op.n_terms).host.stats.get("mode", "program")}
+    rhs = torch.as_tensor(b.forward_rhs().ravel()).cuda()
+    for n_tau in (n_taus or [b.n_terms]):
+        for ls in lead_solvers:
+            t0 = time.perf_counter()
+            _, sweep = build_sweep(cp, b.stiffness, b.partition, n_tau, lead_solver=ls, mass=b.mass)
+            sweep.apply_device(x)
+            torch.cuda.synchronize()
+            t_setup = time.perf_counter() - t0
+            apply_op = lambda v: kron_apply(op, v.view(shape)).reshape(-1)
+            apply_pr = lambda v, sw=sweep: sw.apply_device(v.view(shape)).reshape(-1)
+            times = []
+            for _ in range(2):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                xs, rep = cg(apply_op, apply_pr, rhs, FgmresConfig(tol=1e-8))
+                torch.cuda.synchronize()
+                times.append(time.perf_counter() - t0)
+            res = float(torch.linalg.vector_norm(rhs - apply_op(xs)) / torch.linalg.vector_norm(rhs))
+            sfx = "" if ls == "lu" else f"[{ls}]"
+            out[f"hgs_cg{sfx} n_tau={n_tau}"] = {"iterations": rep.iterations, "converged": bool(rep.converged),
+                                                "seconds": times[1], "first_solve_seconds": times[0],
+                                                "setup_seconds": t_setup, "true_rel_residual": res, "tol": 1e-8}
+    return out
+
+
 def apply_breakdown(cfg_id, beta=1e-2):
     """one KKT matvec (GB/s vs the HBM floor) and one hGSoc apply
     split into its coupling launches and P~ solves, LU and fastdiag leads
@@ -580,6 +630,8 @@ def run_ours(args):
                                           f"{dt:.2f} s); NumPy/SciPy oracle port of sgkkt kron_apply, 1 core (GIL-bound)"}
     if rank == 0 and not args.no_solve:
         solves = {"cfg2": solve_block(2, [1e-2])}
+        solves["cfg1_forward"] = forward_block(1)
+        solves["cfg3_forward"] = forward_block(3, [1, 7, 924])
         if not args.no_solve_cfg5:
             solves["cfg5"] = solve_block(5, [1e-2, 1e-4, 1e-6])
             solves["cfg5_apply_breakdown"] = apply_breakdown(5)

@@ -385,7 +385,9 @@ def stencil9_warps(n_groups: int, n_chunks: int) -> int:
     """Warps per CTA for stencil9_kernel: one per column group (resident V
     registers) and at most 16 gather chunks per warp; 8 at most, 16 for
     programs with 9..16 groups."""
-    w = max(1, n_groups, -(-n_chunks // 16))
+    # gather-heavy programs (few column groups, many output chunks) get up to
+    # 8 warps so each gathers <= 4 chunks
+    w = max(1, n_groups, -(-n_chunks // 16), min(8, -(-n_chunks // 4)))
     if S9_BIG and 8 < n_groups <= 16:
         return min(16, w)
     return min(8, w)
