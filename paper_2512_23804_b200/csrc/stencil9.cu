@@ -50,6 +50,11 @@ __host__ __device__ inline Smem9 smem9_layout(int n_slices, const sgk_program9& 
   return s;
 }
 
+template <typename T>
+__device__ __forceinline__ T sel4(T a, T b, T c, T d, int i) {
+  return i == 0 ? a : (i == 1 ? b : (i == 2 ? c : d));
+}
+
 // single accumulation chain: 1 DMUL + 8 DFMA, no extra adds on the FP64 pipe
 __device__ __forceinline__ double dot9(const double (&a)[10], const double (&v)[9]) {
   double u = a[0] * v[0];
@@ -361,12 +366,21 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
           if (irow != nullptr) y = fma(beta.s[0], irow[oc], y);
           orow[oc] = y;
         } else {
+          // per-lane output index: select the view fields by value (a
+          // reference into the parameter views with a per-lane index makes
+          // the compiler copy them to local memory on every output)
           const int o = oc >> 24, k = oc & 0xFFFFFF;
-          double y = pick_s(alpha, o) * acc;
-          const sgk_view& iv = pick(init, o);
-          if (iv.ptr != nullptr) y += pick_s(beta, o) * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
-          const sgk_view& ov = pick(out, o);
-          ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
+          const double al = sel4(alpha.s[0], alpha.s[1], alpha.s[2], alpha.s[3], o);
+          const double be = sel4(beta.s[0], beta.s[1], beta.s[2], beta.s[3], o);
+          const double* ip = sel4(init.v[0].ptr, init.v[1].ptr, init.v[2].ptr, init.v[3].ptr, o);
+          const int64_t il = sel4(init.v[0].ld, init.v[1].ld, init.v[2].ld, init.v[3].ld, o);
+          const int ic = sel4(init.v[0].col0, init.v[1].col0, init.v[2].col0, init.v[3].col0, o);
+          double* op = sel4(out.v[0].ptr, out.v[1].ptr, out.v[2].ptr, out.v[3].ptr, o);
+          const int64_t ol = sel4(out.v[0].ld, out.v[1].ld, out.v[2].ld, out.v[3].ld, o);
+          const int occ = sel4(out.v[0].col0, out.v[1].col0, out.v[2].col0, out.v[3].col0, o);
+          double y = al * acc;
+          if (ip != nullptr) y += be * ip[(int64_t)row * il + ic + k];
+          op[(int64_t)row * ol + occ + k] = y;
         }
       }
     }
