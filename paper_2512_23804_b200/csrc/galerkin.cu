@@ -26,6 +26,11 @@
 
 namespace sgk {
 
+template <typename T>
+__device__ __forceinline__ T sel4v(T a, T b, T c, T d, int i) {
+  return i == 0 ? a : (i == 1 ? b : (i == 2 ? c : d));
+}
+
 constexpr int kChunk = 9;          // stencil entries held in registers per pass
 // the row's t-stacked coefficients are staged in shared memory when they fit
 // next to the U slots (many-term programs: config 3 has 924 slices x 9
@@ -202,11 +207,17 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
       if (c < prog.n_out_cols) {
         const int oc = __ldg(prog.out_col + c);
         const int o = oc >> 24, k = oc & 0xFFFFFF;
-        double y = pick_s(alpha, o) * acc[r];
-        const sgk_view& iv = pick(init, o);
-        if (iv.ptr != nullptr) y += pick_s(beta, o) * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
-        const sgk_view& ov = pick(out, o);
-        ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
+        // view fields selected by value (a per-thread index into the
+        // parameter views would copy them to local memory)
+        const double* ip = sel4v(init.v[0].ptr, init.v[1].ptr, init.v[2].ptr, init.v[3].ptr, o);
+        double* op = sel4v(out.v[0].ptr, out.v[1].ptr, out.v[2].ptr, out.v[3].ptr, o);
+        double y = sel4v(alpha.s[0], alpha.s[1], alpha.s[2], alpha.s[3], o) * acc[r];
+        if (ip != nullptr)
+          y += sel4v(beta.s[0], beta.s[1], beta.s[2], beta.s[3], o) *
+               ip[(int64_t)row * sel4v(init.v[0].ld, init.v[1].ld, init.v[2].ld, init.v[3].ld, o) +
+                  sel4v(init.v[0].col0, init.v[1].col0, init.v[2].col0, init.v[3].col0, o) + k];
+        op[(int64_t)row * sel4v(out.v[0].ld, out.v[1].ld, out.v[2].ld, out.v[3].ld, o) +
+           sel4v(out.v[0].col0, out.v[1].col0, out.v[2].col0, out.v[3].col0, o) + k] = y;
       }
     }
   }
