@@ -77,6 +77,12 @@ typedef struct {
   const int32_t* gather_slot; /* phase-local slot (step-step0)*32+lane      */
   const double* gather_coef;
   const int32_t* out_col;     /* [n_out_cols] (output<<24)|column           */
+  /* compact gather (optional, NULL = use gather_slot/gather_coef): word e =
+   * gather_slot[e] | (index of gather_coef[e] in coef_tab) << 16           */
+  int32_t n_coef;             /* <= 2048 distinct coefficients              */
+  int32_t pad;
+  const uint32_t* gather_word;
+  const double* coef_tab;
 } sgk_program;
 
 /* Strided view of a node-major (n_rows x ld) fp64 block, columns

@@ -64,6 +64,10 @@ class Program(ctypes.Structure):
         ("gather_slot", c_vp),
         ("gather_coef", c_vp),
         ("out_col", c_vp),
+        ("n_coef", c_i32),
+        ("pad", c_i32),
+        ("gather_word", c_vp),
+        ("coef_tab", c_vp),
     ]
 
 

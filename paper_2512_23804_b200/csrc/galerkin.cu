@@ -48,6 +48,10 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
   extern __shared__ double smem[];
   double* coef_s = smem;                          // [stage_n] when STAGED
   double* ubuf = smem + (STAGED ? stage_n : 0);    // U slots of one phase
+  // compact gather: the small coefficient table is read through L1 (it
+  // stays resident; no shared memory next to the staged block)
+  const bool compact = prog.gather_word != nullptr;
+  const double* __restrict__ ctab = prog.coef_tab;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -157,17 +161,33 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
           const int e0 = __ldg(gp + c), e1 = __ldg(gp + c + 1);
           double a0 = acc[0], a1 = 0.0, a2 = 0.0, a3 = 0.0;
           int e = e0 + r;
-          for (; e + 3 * parts < e1; e += 4 * parts) {
-            const int s0 = __ldg(prog.gather_slot + e), s1 = __ldg(prog.gather_slot + e + parts);
-            const int s2 = __ldg(prog.gather_slot + e + 2 * parts), s3 = __ldg(prog.gather_slot + e + 3 * parts);
-            const double h0 = __ldg(prog.gather_coef + e), h1 = __ldg(prog.gather_coef + e + parts);
-            const double h2 = __ldg(prog.gather_coef + e + 2 * parts), h3 = __ldg(prog.gather_coef + e + 3 * parts);
-            a0 = fma(h0, ubuf[s0], a0);
-            a1 = fma(h1, ubuf[s1], a1);
-            a2 = fma(h2, ubuf[s2], a2);
-            a3 = fma(h3, ubuf[s3], a3);
+          if (compact) {
+            for (; e + 3 * parts < e1; e += 4 * parts) {
+              const uint32_t w0 = __ldg(prog.gather_word + e), w1 = __ldg(prog.gather_word + e + parts);
+              const uint32_t w2 = __ldg(prog.gather_word + e + 2 * parts);
+              const uint32_t w3 = __ldg(prog.gather_word + e + 3 * parts);
+              a0 = fma(__ldg(ctab + (w0 >> 16)), ubuf[w0 & 0xFFFF], a0);
+              a1 = fma(__ldg(ctab + (w1 >> 16)), ubuf[w1 & 0xFFFF], a1);
+              a2 = fma(__ldg(ctab + (w2 >> 16)), ubuf[w2 & 0xFFFF], a2);
+              a3 = fma(__ldg(ctab + (w3 >> 16)), ubuf[w3 & 0xFFFF], a3);
+            }
+            for (; e < e1; e += parts) {
+              const uint32_t w0 = __ldg(prog.gather_word + e);
+              a0 = fma(__ldg(ctab + (w0 >> 16)), ubuf[w0 & 0xFFFF], a0);
+            }
+          } else {
+            for (; e + 3 * parts < e1; e += 4 * parts) {
+              const int s0 = __ldg(prog.gather_slot + e), s1 = __ldg(prog.gather_slot + e + parts);
+              const int s2 = __ldg(prog.gather_slot + e + 2 * parts), s3 = __ldg(prog.gather_slot + e + 3 * parts);
+              const double h0 = __ldg(prog.gather_coef + e), h1 = __ldg(prog.gather_coef + e + parts);
+              const double h2 = __ldg(prog.gather_coef + e + 2 * parts), h3 = __ldg(prog.gather_coef + e + 3 * parts);
+              a0 = fma(h0, ubuf[s0], a0);
+              a1 = fma(h1, ubuf[s1], a1);
+              a2 = fma(h2, ubuf[s2], a2);
+              a3 = fma(h3, ubuf[s3], a3);
+            }
+            for (; e < e1; e += parts) a0 = fma(__ldg(prog.gather_coef + e), ubuf[__ldg(prog.gather_slot + e)], a0);
           }
-          for (; e < e1; e += parts) a0 = fma(__ldg(prog.gather_coef + e), ubuf[__ldg(prog.gather_slot + e)], a0);
           acc[0] = (a0 + a1) + (a2 + a3);
         }
       } else {
