@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import math
 import time
+import weakref
 
 import numpy as np
 import scipy.sparse as sp
@@ -35,9 +36,10 @@ from .random_field import CovarianceSpec, kl_expand
 
 __all__ = ["attached_pattern", "build_problem_device", "lognormal_fields_device"]
 
-# id(host matrix) -> (matrix, device pattern, slice index): host matrices that
-# are views of a device-assembled pattern
-_SLICES: dict[int, tuple[object, DevicePattern, int]] = {}
+# id(host matrix) -> (weak ref to the matrix, device pattern, slice index):
+# host matrices that are views of a device-assembled pattern; entries go away
+# with their matrices
+_SLICES: dict[int, tuple[weakref.ref, DevicePattern, int]] = {}
 
 
 def attached_pattern(mats) -> DevicePattern | None:
@@ -46,7 +48,7 @@ def attached_pattern(mats) -> DevicePattern | None:
     pat = None
     for t, m in enumerate(mats):
         hit = _SLICES.get(id(m))
-        if hit is None or hit[0] is not m or hit[2] != t or (pat is not None and hit[1] is not pat):
+        if hit is None or hit[0]() is not m or hit[2] != t or (pat is not None and hit[1] is not pat):
             return None
         pat = hit[1]
     return pat
@@ -113,7 +115,8 @@ def build_problem_device(cfg, *, n: int | None = None, kl_method: str = "separab
     ip, ix = pat.indptr.astype(np.int32), pat.indices.astype(np.int32)
     mats = [sp.csr_matrix((data[t], ix, ip), shape=(pat.n_rows, pat.n_rows)) for t in range(T + 1)]
     for t, m in enumerate(mats):
-        _SLICES[id(m)] = (m, pat, t)
+        _SLICES[id(m)] = (weakref.ref(m), pat, t)
+        weakref.finalize(m, _SLICES.pop, id(m), None)
     if gpc is None:
         host_fields = fields.cpu().numpy()
         gpc = GpcCoefficientField(coeff_fields=[fem.CoefficientField(values=v) for v in host_fields])

@@ -19,6 +19,7 @@ All sweeps run on one stream without host synchronisation.
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass, field
 from typing import Callable
 
@@ -116,14 +117,19 @@ class _DeviceMass:
         return x.reshape(b.shape)
 
 
-_MASS_CACHE: dict[int, tuple[csr_matrix, _DeviceMass]] = {}
+# device copies of mass matrices used by chebyshev_mass_solve, keyed by the
+# matrix object; an entry (and its device buffers) is dropped when the matrix
+# is garbage-collected
+_MASS_CACHE: dict[int, tuple[weakref.ref, _DeviceMass]] = {}
 
 
 def _device_mass(mass: csr_matrix) -> _DeviceMass:
-    hit = _MASS_CACHE.get(id(mass))
-    if hit is None or hit[0] is not mass:
-        hit = (mass, _DeviceMass(mass))
-        _MASS_CACHE[id(mass)] = hit
+    key = id(mass)
+    hit = _MASS_CACHE.get(key)
+    if hit is None or hit[0]() is not mass:
+        hit = (weakref.ref(mass), _DeviceMass(mass))
+        _MASS_CACHE[key] = hit
+        weakref.finalize(mass, _MASS_CACHE.pop, key, None)
     return hit[1]
 
 
