@@ -98,11 +98,22 @@ extern "C" int sgk_fastdiag_solve(const sgk_fastdiag* fd, const sgk_segview* b, 
   // cuBLAS is column-major: a row-major (rows x width, ld) block is a
   // column-major (width x rows, ld) matrix.  fd->st (row-major S^T) is S in
   // column-major order, fd->s (row-major S) is S^T in column-major order.
-  for (int s = 0; s < fd->n_seg; ++s) {
+  // segments stacked at a uniform stride (the Krylov vector's y/u/lambda
+  // blocks) run each of passes 1 and 4 as ONE strided batch over
+  // (segment, grid line): segment s, line i sits at (s*n + i)*n*ld
+  auto stacked = [&](const sgk_segview* v) {
+    if (fd->n_seg == 1) return true;
+    const int64_t st = n2 * v->ld;
+    for (int s = 1; s < fd->n_seg; ++s)
+      if (v->ptr[s] - v->ptr[s - 1] != st) return false;
+    return true;
+  };
+  const int lines_b = stacked(b) ? fd->n_seg * n : n;
+  for (int s = 0; s < fd->n_seg; s += lines_b / n) {
     // pass 1: T1[iy][b][k] = sum_ix S[ix,b] X[iy*n+ix][k]      (batch over iy)
     if (int rc = blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, width, n, n, &one,
                                                       b->ptr[s] + b->col0, (int)b->ld, (long long)n * b->ld, fd->st,
-                                                      n, 0, &zero, t1 + s * seg, width, (long long)nw, n),
+                                                      n, 0, &zero, t1 + s * seg, width, (long long)nw, lines_b),
                             "pass 1"))
       return rc;
   }
@@ -131,11 +142,12 @@ extern "C" int sgk_fastdiag_solve(const sgk_fastdiag* fd, const sgk_segview* b, 
                                                     fd->n_seg),
                           "pass 3"))
     return rc;
-  for (int s = 0; s < fd->n_seg; ++s) {
+  const int lines_x = stacked(x) ? fd->n_seg * n : n;
+  for (int s = 0; s < fd->n_seg; s += lines_x / n) {
     // pass 4: X[iy*n+ix][k] = sum_b S[ix,b] T1[iy][b][k]
     if (int rc = blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, width, n, n, &one, t1 + s * seg,
                                                       width, (long long)nw, fd->s, n, 0, &zero, x->ptr[s] + x->col0,
-                                                      (int)x->ld, (long long)n * x->ld, n),
+                                                      (int)x->ld, (long long)n * x->ld, lines_x),
                             "pass 4"))
       return rc;
   }

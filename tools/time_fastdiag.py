@@ -75,3 +75,15 @@ for lo, hi in ranges:
     segs = [(outs[0], lo)]
     ts = timed(lambda: lead.solve_segments(segs, segs, hi - lo))
     print(f"  A~ solve width {hi - lo:4d}: {ts:.3f} ms ({8.0 * (hi - lo) * n ** 3 / (ts * 1e-3) / 1e12:.1f} TFLOP/s)")
+# stacked segments (one Krylov vector's y/u/lambda blocks): passes 1 and 4 as one batch
+stack = torch.empty((3, sys_.n_h, sys_.n_xi), dtype=torch.float64, device="cuda")
+sb = [stack[i] for i in range(3)]
+tot = 0.0
+for lo, hi in ranges:
+    segs = [(t_, lo) for t_ in sb]
+    tot += timed(lambda: fac.solve_segments(segs, segs, hi - lo))
+sep = 0.0
+for lo, hi in ranges:
+    segs = [(t_, lo) for t_ in outs]
+    sep += timed(lambda: fac.solve_segments(segs, segs, hi - lo))
+print(f"P~ solves over the 5 levels: separate segments {sep:.3f} ms, stacked segments {tot:.3f} ms")
