@@ -20,7 +20,11 @@
 
 namespace sgk {
 
-constexpr int kCols = 4;  // column slots per lane
+#ifndef SGK_S9_KC
+#define SGK_S9_KC 4
+#endif
+constexpr int kCols = SGK_S9_KC;       // column slots per lane
+constexpr int kGroupCols = 32 * kCols;  // columns of one group (one warp)
 #ifndef SGK_VLD
 #define SGK_VLD __ldg
 #endif
@@ -146,10 +150,10 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
   int rbase = 0, rq0 = 0, rq1 = 0;
   const double* rvb = nullptr;
   int64_t rld = 0;
-  int rncols = 128;
+  int rncols = kGroupCols;
   double rv[kCols][9];
   if (RESIDENT && warp < prog.n_groups) {
-    for (int g = 0; g < warp; ++g) rbase += 128 * (groups[4 * (g + 1) + 3] - groups[4 * g + 3]);
+    for (int g = 0; g < warp; ++g) rbase += kGroupCols * (groups[4 * (g + 1) + 3] - groups[4 * g + 3]);
     const int4 gi = *reinterpret_cast<const int4*>(groups + 4 * warp);
     rq0 = gi.w;
     rq1 = groups[4 * (warp + 1) + 3];
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
   }
   auto load_v = [&](int r, double (&v)[kCols][9]) {
     const int32_t* cg = pat.colind9 + (int64_t)r * 9;
-    if (rncols == 128) {  // common case: immediate offsets 0/256/512/768 bytes
+    if (rncols == kGroupCols) {  // common case: immediate offsets 0/256/... bytes
       const double* b = rvb + lane;
 #pragma unroll
       for (int jj = 0; jj < 9; ++jj) {
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
           p01 = a2[0];
           p23 = a2[1];
         }
-        for (int q = rq0; q < rq1; ++q, ubq += 128) {
+        for (int q = rq0; q < rq1; ++q, ubq += kGroupCols) {
           const int rec = recn;
           double* ub = ubq + (lane ^ (rec >> 16));  // swizzled slot, conflict-free STS
           double a[10];
@@ -249,10 +253,8 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
             p23 = a2[1];
           }
           // slot (q, c, lane) = base + 128 q + 32 c + (lane ^ sw_q)
-          ub[0] = dot9(a, rv[0]);
-          ub[32] = dot9(a, rv[1]);
-          ub[64] = dot9(a, rv[2]);
-          ub[96] = dot9(a, rv[3]);
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) ub[32 * c] = dot9(a, rv[c]);
         }
         if (next < r_end) {  // prefetch: overlaps barrier + gather
           const int32_t* cn = pat.colind9 + (int64_t)next * 9;
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
               for (int c = 0; c < kCols; ++c) {
                 rv[c][3 * line] = rv[c][3 * line + 1];
                 rv[c][3 * line + 1] = rv[c][3 * line + 2];
-                rv[c][3 * line + 2] = __ldg(vr + (rncols == 128 ? 32 * c : min(32 * c, rncols - 1 - lane)));
+                rv[c][3 * line + 2] = __ldg(vr + (rncols == kGroupCols ? 32 * c : min(32 * c, rncols - 1 - lane)));
               }
             }
           } else {
@@ -281,14 +283,14 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
     } else {
     int ubase = 0;  // slot base of group g: 128 slots per step, groups in order
     for (int g = 0; g < warp && g < prog.n_groups; ++g)
-      ubase += 128 * (groups[4 * (g + 1) + 3] - groups[4 * g + 3]);
+      ubase += kGroupCols * (groups[4 * (g + 1) + 3] - groups[4 * g + 3]);
     for (int g = warp; g < prog.n_groups; g += nwarps) {
       const int4 gi = *reinterpret_cast<const int4*>(groups + 4 * g);
       const int q1 = groups[4 * (g + 1) + 3];
       const double* vbase = in_ptr[gi.x] + gi.y;
       const int64_t vld = in_ld[gi.x];
       double v[kCols][9];
-      if (gi.z == 128) {
+      if (gi.z == kGroupCols) {
         const double* base = vbase + lane;
 #pragma unroll
         for (int jj = 0; jj < 9; ++jj) {
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
         }
       }
       double* ubq = ubuf + ubase;
-      for (int q = gi.w; q < q1; ++q, ubq += 128) {
+      for (int q = gi.w; q < q1; ++q, ubq += kGroupCols) {
         const int rec = steps[q];
         double* ub = ubq + (lane ^ (rec >> 16));
         const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (rec & 0xFFFF));
@@ -316,14 +318,12 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
           a[2 * k] = p.x;
           a[2 * k + 1] = p.y;
         }
-        ub[0] = dot9(a, v[0]);
-        ub[32] = dot9(a, v[1]);
-        ub[64] = dot9(a, v[2]);
-        ub[96] = dot9(a, v[3]);
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) ub[32 * c] = dot9(a, v[c]);
       }
       // skip the slots of the groups owned by the other warps
       for (int g2 = g; g2 < g + nwarps && g2 < prog.n_groups; ++g2)
-        ubase += 128 * (groups[4 * (g2 + 1) + 3] - groups[4 * g2 + 3]);
+        ubase += kGroupCols * (groups[4 * (g2 + 1) + 3] - groups[4 * g2 + 3]);
     }
     }
 

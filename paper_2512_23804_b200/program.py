@@ -373,7 +373,9 @@ class HostProgram9:
     warps: int = 1  # CTA warps the gather layout assumes (chunk c -> warp c % warps)
 
 
-GROUP_COLS = 128  # 4 column slots x 32 lanes
+# 4 column slots x 32 lanes (SGKKT_S9_KC selects another slot count; the
+# library must be built with the same -DSGK_S9_KC)
+GROUP_COLS = 32 * int(os.environ.get("SGKKT_S9_KC", "4"))
 
 
 # up to 16 warps (one 512-thread CTA per SM) so programs with 9..16 column
@@ -789,7 +791,7 @@ def emulate9(prog: HostProgram9, mats, inputs, inits, alpha, beta):
         x = inputs[s]
         for q in range(q0, q1):
             t, sw = int(prog.step_rec[q]) & 0xFFFF, int(prog.step_rec[q]) >> 16
-            for c in range(4):
+            for c in range(GROUP_COLS // 32):
                 for lane in range(32):
                     col = col0 + min(32 * c + lane, ncols - 1)
                     ub[:, base + (q - q0) * GROUP_COLS + c * 32 + (lane ^ sw)] = mats[t] @ x[:, col]
