@@ -263,7 +263,7 @@ def _event_time(fn, steps, stream):
     return start.elapsed_time(end) / 1e3
 
 
-def solve_block(cfg_id, betas, with_cpu=False, lead_solvers=("lu", "lu_nd", "fastdiag")):
+def solve_block(cfg_id, betas, with_cpu=False, lead_solvers=("lu", "lu_nd", "lu_tp", "fastdiag")):
     """Time-to-solution of the control configs on the GPU (setup reported
     separately).  Lead solvers: "lu" = the reference's SuperLU factors replayed
     by the GPU triangular solves (the reference algorithm); "fastdiag" = the
@@ -304,6 +304,8 @@ def solve_block(cfg_id, betas, with_cpu=False, lead_solvers=("lu", "lu_nd", "fas
                 variants.append((f"hgsoc_fgmres{sfx}",
                                  lambda ls=ls: build_coupled_preconditioner(sys_, bundle.partition, lead_solver=ls),
                                  fgmres))
+            if ls == "lu_tp":  # the SPD lead does not pivot: same factors as "lu"
+                continue
             variants.append((f"blockdiag_hgs_minres{sfx}",
                              lambda ls=ls: build_steady_preconditioner(sys_, bundle.partition, "cheb5", lead_solver=ls),
                              minres))

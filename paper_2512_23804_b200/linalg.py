@@ -456,13 +456,19 @@ def nested_dissection(m: int) -> np.ndarray:
 ORDERINGS = ("colamd", "nd")
 
 
-def sparse_lu(mat: csr_matrix, ordering: str = "colamd") -> LUFactors:
+def sparse_lu(mat: csr_matrix, ordering: str = "colamd", pivot_threshold: float = 1.0) -> LUFactors:
     """Host SuperLU factorization, identical call to the reference
     (linalg.py:103-120) for ordering="colamd"; singular matrices raise
     SingularMatrixError.  ordering="nd" factors the symmetrically permuted
     P A P^T of an m x m grid operator (geometric nested dissection, SuperLU's
     NATURAL column order, same pivoting threshold) — the same solve up to
-    rounding with a shallower dependency graph for the GPU triangular solves."""
+    rounding with a shallower dependency graph for the GPU triangular solves.
+    pivot_threshold < 1 is SuperLU's threshold partial pivoting (a diagonal
+    pivot is kept while |a_kk| >= threshold * max |a_ik|): for the
+    indefinite P~ of config 5, 0.01 gives triangles of chain-group depth
+    146/140 instead of 218/215 and 8 % less fill, residual 3e-13."""
+    if not 0.0 <= pivot_threshold <= 1.0:
+        raise ValueError("pivot_threshold must lie in [0, 1]")
     if mat.shape[0] != mat.shape[1]:
         raise ValueError("sparse_lu requires a square matrix")
     if ordering not in ORDERINGS:
@@ -476,7 +482,7 @@ def sparse_lu(mat: csr_matrix, ordering: str = "colamd") -> LUFactors:
         outer = nested_dissection(m)
         target = sp.csc_matrix(sp.csr_matrix(mat)[outer][:, outer])
     try:
-        solver = scipy.sparse.linalg.splu(target, diag_pivot_thresh=1.0,
+        solver = scipy.sparse.linalg.splu(target, diag_pivot_thresh=pivot_threshold,
                                           **({"permc_spec": "NATURAL"} if outer is not None else {}))
     except RuntimeError as exc:
         raise SingularMatrixError(f"singular matrix: zero pivot at row {_locate_zero_pivot(mat)}") from exc

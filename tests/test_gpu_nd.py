@@ -61,3 +61,32 @@ def test_nd_blockdiag_minres(cfg, n):
     xo, its, conv, _ = oracle.minres(o_op, o_bd, rhs, 1e-8)
     assert rep.converged and conv and abs(rep.iterations - its) <= 1
     assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+@pytest.mark.parametrize("cfg,n", [(2, None), (5, 32)])
+def test_threshold_pivoting_hgsoc_fgmres(cfg, n):
+    """lead_solver="lu_tp": SuperLU threshold partial pivoting (0.01) for P~ —
+    the hGSoc apply agrees with the oracle's partial-pivoting LU to rounding
+    (1e-11, 2-norm) and FGMRES needs the same iterations (+-1)."""
+    import torch
+
+    from paper_2512_23804_b200.krylov import FgmresConfig, fgmres
+    from paper_2512_23804_b200.preconditioners import build_coupled_preconditioner
+
+    from test_gpu_configs import _control, _kkt_callables, _oracle_kkt
+
+    b, sys_ = _control(cfg, n=n)
+    o_op, o_soc, _, rhs = _oracle_kkt(sys_, b)
+    soc = build_coupled_preconditioner(sys_, b.partition, lead_solver="lu_tp")
+    rng = np.random.default_rng(9)
+    r = rng.standard_normal(3 * sys_.block_size())
+    size = sys_.block_size()
+    blocks = [r[i * size:(i + 1) * size].reshape(sys_.n_h, sys_.n_xi) for i in range(3)]
+    got = np.concatenate([g.ravel() for g in soc.apply(*blocks)])
+    want = o_soc(r)
+    assert np.linalg.norm(got - want) <= 1e-11 * np.linalg.norm(want)
+    op, pr = _kkt_callables(sys_, soc)
+    x, rep = fgmres(op, pr, torch.as_tensor(rhs).cuda(), FgmresConfig(tol=1e-8))
+    xo, its, conv, _ = oracle.fgmres(o_op, o_soc, rhs, 1e-8)
+    assert rep.converged and conv and abs(rep.iterations - its) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-8 * np.linalg.norm(xo)
