@@ -578,6 +578,24 @@ def run_ours(args):
     e2e_err = float(np.abs(wp.numpy() - w.cpu().numpy()).max())
     t_e2e = reduce_max(t_e2e, dev)
     e2e_value = whole_job_gbs(B, e2e_steps, ws, t_e2e)
+    # the PCIe roofline of the e2e path on this box: both directions of the
+    # step's copies running concurrently (raw copies, no kernel)
+    yd = torch.empty_like(x)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def duplex():
+        with torch.cuda.stream(s1):
+            x.copy_(xp, non_blocking=True)
+        with torch.cuda.stream(s2):
+            wp.copy_(yd, non_blocking=True)
+        stream.wait_stream(s1)
+        stream.wait_stream(s2)
+
+    duplex()
+    torch.cuda.synchronize()
+    t_dup = _event_time(duplex, 3, stream) / 3
+    pcie = {"duplex_copy_ms": t_dup * 1e3, "duplex_gbs": 2 * xp.numel() * 8 / t_dup / 1e9,
+            "frac_of_duplex_copy_time": t_dup / (t_e2e / e2e_steps)}
 
     peak, peak_kind = _peaks()
     achieved = B / kernel_avg / 1e9
@@ -608,7 +626,7 @@ def run_ours(args):
                    "spot_check_rel_err_vs_oracle": spot_err},
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": int(x.numel() * 8),
                 "d2h_bytes_per_step": int(w.numel() * 8), "api": "kron_apply(op, pinned CPU tensor, out=pinned)",
-                "max_abs_diff_vs_device": e2e_err},
+                "max_abs_diff_vs_device": e2e_err, "pcie_roofline": pcie},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind,
