@@ -190,8 +190,22 @@ def compile_program(
                 nsteps = len(g[0][1])
                 lanes = [it[0] for it in g] + [-1] * (32 - len(g))
                 steps = -np.ones((nsteps, 32), np.int64)
-                for lane, (_, terms) in enumerate(g):
-                    steps[: len(terms), lane] = terms
+                # each lane's terms may run in any order: at every step pick,
+                # lane by lane, the remaining term whose coefficients sit in the
+                # least-used shared-memory bank pair (the row block is staged
+                # as t*9 + jj doubles: bank pair (9 t) mod 16), so the per-lane
+                # coefficient loads of a step conflict less (config 3: 5.9 ->
+                # 3.0 wavefronts per load on average, ideal 2)
+                remaining = [list(terms) for _, terms in g]
+                for q in range(nsteps):
+                    used = np.zeros(16, np.int64)
+                    for lane, rem in enumerate(remaining):
+                        if not rem:
+                            continue
+                        k = min(range(len(rem)), key=lambda i: (used[(rem[i] * 9) % 16], i))
+                        t = rem.pop(k)
+                        steps[q, lane] = t
+                        used[(t * 9) % 16] += 1
                 groups.append((lanes, steps))
         else:
             chosen = "uniform"
