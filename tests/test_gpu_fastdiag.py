@@ -162,3 +162,25 @@ def test_control_solves_fastdiag_vs_oracle(cfg, n, beta):
     xo2, its2, conv2, _ = oracle.minres(o_op, o_bd, rhs, 1e-8)
     assert rep2.converged and conv2 and abs(rep2.iterations - its2) <= 1, (rep2.iterations, its2)
     assert np.linalg.norm(x2.cpu().numpy() - xo2) <= 1e-8 * np.linalg.norm(xo2)
+
+
+def test_stacked_segments_match_separate_segments():
+    """P~ solves on the y/u/lambda blocks of one stacked buffer (passes 1 and 4
+    batched over all three segments) equal the per-segment path."""
+    import torch
+
+    from paper_2512_23804_b200.fastdiag import fastdiag_kkt_factor
+    from paper_2512_23804_b200.problems import build_problem, steady_system
+
+    b = build_problem(2)
+    sys_ = steady_system(b)
+    f = fastdiag_kkt_factor(sys_.stiffness[0], sys_.mass, sys_.beta)
+    rng = np.random.default_rng(21)
+    stack = torch.as_tensor(rng.standard_normal((3, sys_.n_h, sys_.n_xi))).cuda()
+    sep = [stack[i].clone() for i in range(3)]
+    for lo, hi in b.partition.ranges():
+        f.solve_segments([(stack[i], lo) for i in range(3)], [(stack[i], lo) for i in range(3)], hi - lo)
+        f.solve_segments([(t, lo) for t in sep], [(t, lo) for t in sep], hi - lo)
+    got = stack.cpu().numpy()
+    want = np.stack([t.cpu().numpy() for t in sep])
+    assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
