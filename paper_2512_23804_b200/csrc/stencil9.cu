@@ -16,6 +16,8 @@
 //     so per row only the U values move through shared memory.
 // Rows are processed grid-stride by persistent CTAs; the row's coefficient
 // block (n_slices x 10 doubles) is staged with 16-byte loads.
+#include <cstdlib>
+
 #include "sgk_common.cuh"
 
 namespace sgk {
@@ -388,6 +390,251 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
   cp_async_wait1();
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised variant (resident programs with <= 8 column groups, e.g.
+// the config-4 matvec): warps 0..7 produce the U values of row n into U
+// buffer n&1 while warps 8..15 gather row n-1 from the other buffer.  Named
+// barriers replace the two block-wide barriers per row:
+//   FULL[b]  (ids 1,2): producers arrive after writing buffer b, consumers sync;
+//   EMPTY[b] (ids 3,4): consumers arrive after reading buffer b, producers sync
+//                       before overwriting it two rows later;
+//   PROD     (id 5)   : producers only (coefficient staging hand-over).
+// The products of one row and the gather of the previous one overlap instead
+// of alternating.  Same arithmetic as stencil9_kernel (bit-identical).
+__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__host__ __device__ inline Smem9 smem9_ws_layout(int n_slices, const sgk_program9& p) {
+  Smem9 s = smem9_layout(n_slices, p);
+  const size_t extra = align16(sizeof(double) * ((size_t)p.n_ubuf + 64));  // second U buffer
+  s.steps += extra;
+  s.groups += extra;
+  s.ccnt += extra;
+  s.coff += extra;
+  s.gent += extra;
+  s.total += extra;
+  return s;
+}
+
+template <int MAXOUT, bool ONEOUT>
+__global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
+                                                            ViewSet out, ViewSet init, ScalarSet alpha,
+                                                            ScalarSet beta) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const Smem9 L = smem9_ws_layout(pat.n_slices, prog);
+  double* coef_s = reinterpret_cast<double*>(sm + L.coef);
+  double* ubuf = reinterpret_cast<double*>(sm + L.ubuf);
+  double* ctab = reinterpret_cast<double*>(sm + L.ctab);
+  int32_t* steps = reinterpret_cast<int32_t*>(sm + L.steps);
+  int32_t* groups = reinterpret_cast<int32_t*>(sm + L.groups);
+  int32_t* ccnt = reinterpret_cast<int32_t*>(sm + L.ccnt);
+  int32_t* coff = reinterpret_cast<int32_t*>(sm + L.coff);
+  uint32_t* gent = reinterpret_cast<uint32_t*>(sm + L.gent);
+  const int ustride = (int)(align16(sizeof(double) * ((size_t)prog.n_ubuf + 64)));  // bytes between U buffers
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const bool producer = warp < 8;
+  const int n_chunks = prog.n_chunks;
+  __shared__ const double* in_ptr[SGK_MAX_IO];
+  __shared__ int64_t in_ld[SGK_MAX_IO];
+  if (tid < SGK_MAX_IO) {
+    const sgk_view& vv = pick(in, tid);
+    in_ptr[tid] = vv.ptr + vv.col0;
+    in_ld[tid] = vv.ld;
+  }
+  const int ncoef = pat.n_slices * 10;
+  for (int i = tid; i < prog.n_coef; i += blockDim.x) ctab[i] = prog.coef_tab[i];
+  for (int i = tid; i < prog.n_steps; i += blockDim.x) steps[i] = prog.step_rec[i];
+  for (int i = tid; i < 4 * (prog.n_groups + 1); i += blockDim.x) groups[i] = prog.group_info[i];
+  for (int i = tid; i < n_chunks; i += blockDim.x) {
+    ccnt[i] = prog.gather_ptr[2 * i];
+    coff[i] = prog.gather_ptr[2 * i + 1];
+  }
+  for (int i = tid; i < prog.n_gather; i += blockDim.x) gent[i] = prog.gather_ent[i];
+  for (int i = tid; i < 64; i += blockDim.x) {
+    ubuf[prog.n_ubuf + i] = 0.0;
+    reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ubuf) + ustride)[prog.n_ubuf + i] = 0.0;
+  }
+  __syncthreads();
+
+  const int r_begin = blockIdx.x, r_end = pat.n_rows, r_step = gridDim.x;
+  if (producer) {
+    const int pt = tid;  // 0..255
+    auto stage = [&](int row, int buf) {
+      const double* src = pat.coef10 + (int64_t)row * ncoef;
+      double* dst = coef_s + buf * ncoef;
+      for (int i = pt; i < ncoef / 2; i += 256) cp_async16(dst + 2 * i, src + 2 * i);
+    };
+    int rbase = 0, rq0 = 0, rq1 = 0;
+    const double* rvb = nullptr;
+    int64_t rld = 0;
+    int rncols = kGroupCols;
+    double rv[kCols][9];
+    const bool active = warp < prog.n_groups;
+    if (active) {
+      for (int g = 0; g < warp; ++g) rbase += kGroupCols * (groups[4 * (g + 1) + 3] - groups[4 * g + 3]);
+      const int4 gi = *reinterpret_cast<const int4*>(groups + 4 * warp);
+      rq0 = gi.w;
+      rq1 = groups[4 * (warp + 1) + 3];
+      rvb = in_ptr[gi.x] + gi.y;
+      rld = in_ld[gi.x];
+      rncols = gi.z;
+    }
+    auto load_v = [&](int r) {
+      const int32_t* cg = pat.colind9 + (int64_t)r * 9;
+#pragma unroll
+      for (int jj = 0; jj < 9; ++jj) {
+        const double* vr = rvb + (int64_t)__ldg(cg + jj) * rld;
+#pragma unroll
+        for (int c = 0; c < kCols; ++c)
+          rv[c][jj] = SGK_VLD(vr + (rncols == kGroupCols ? 32 * c + lane : min(32 * c + lane, rncols - 1)));
+      }
+    };
+    int row = r_begin;
+    if (row < r_end) stage(row, 0);
+    cp_async_commit();
+    if (active && row < r_end) load_v(row);
+    int it = 0;
+    for (; row < r_end; row += r_step, ++it) {
+      const int cb = it & 1;
+      const int next = row + r_step;
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      bar_sync_n(5, 256);  // this row's coefficients visible; every producer is done with row it-1
+      if (next < r_end) stage(next, cb ^ 1);
+      cp_async_commit();
+      if (it >= 2) bar_sync_n(3 + cb, 512);  // consumers are done with U buffer cb (row it-2)
+      if (active) {
+        const double* crow = coef_s + cb * ncoef;
+        double* ubq = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ubuf) + cb * ustride) + rbase;
+        int recn = rq0 < rq1 ? steps[rq0] : 0;
+        double2 p01 = make_double2(0.0, 0.0), p23 = p01;
+        if (rq0 < rq1) {
+          const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (recn & 0xFFFF));
+          p01 = a2[0];
+          p23 = a2[1];
+        }
+        for (int q = rq0; q < rq1; ++q, ubq += kGroupCols) {
+          const int rec = recn;
+          double* ub = ubq + (lane ^ (rec >> 16));
+          double a[10];
+          a[0] = p01.x; a[1] = p01.y; a[2] = p23.x; a[3] = p23.y;
+          {
+            const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (rec & 0xFFFF));
+#pragma unroll
+            for (int k = 2; k < 5; ++k) {
+              const double2 p = a2[k];
+              a[2 * k] = p.x;
+              a[2 * k + 1] = p.y;
+            }
+          }
+          recn = steps[q + 1 < rq1 ? q + 1 : q];
+          {
+            const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (recn & 0xFFFF));
+            p01 = a2[0];
+            p23 = a2[1];
+          }
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) ub[32 * c] = dot9(a, rv[c]);
+        }
+      }
+      bar_arrive_n(1 + cb, 512);  // U buffer cb holds row it
+      if (active && next < r_end) load_v(next);  // prefetch: overlaps the next waits
+    }
+    // match the consumers' last EMPTY arrivals
+    for (int k = (it >= 2 ? it - 2 : 0); k < it; ++k) bar_sync_n(3 + (k & 1), 512);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  } else {
+    const int cw = warp - 8;
+    int ocol[MAXOUT];
+#pragma unroll
+    for (int r = 0; r < MAXOUT; ++r) {
+      const int chunk = cw + r * 8;
+      ocol[r] = chunk < n_chunks ? __ldg(prog.out_col + chunk * 32 + lane) : -1;
+    }
+    int it = 0;
+    for (int row = r_begin; row < r_end; row += r_step, ++it) {
+      const int cb = it & 1;
+      bar_sync_n(1 + cb, 512);  // products of this row are in U buffer cb
+      const unsigned char* smb = sm + cb * ustride;  // U addresses of buffer cb
+      double* orow = nullptr;
+      const double* irow = nullptr;
+      if constexpr (ONEOUT) {
+        orow = out.v[0].ptr + (int64_t)row * out.v[0].ld + out.v[0].col0;
+        if (init.v[0].ptr != nullptr) irow = init.v[0].ptr + (int64_t)row * init.v[0].ld + init.v[0].col0;
+      }
+#pragma unroll
+      for (int rb = 0; rb < MAXOUT; ++rb) {
+        const int chunk = cw + rb * 8;
+        if (chunk >= n_chunks) break;
+        const int npair = ccnt[chunk] >> 1;
+        const uint2* gp = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 2
+        for (int e = 0; e < npair; ++e, gp += 32) {
+          const uint2 w = *gp;
+          acc0 = fma(*reinterpret_cast<const double*>(sm + (w.x & 0x3FFF)),
+                     *reinterpret_cast<const double*>(smb + (w.x >> 14)), acc0);
+          acc1 = fma(*reinterpret_cast<const double*>(sm + (w.y & 0x3FFF)),
+                     *reinterpret_cast<const double*>(smb + (w.y >> 14)), acc1);
+        }
+        const int oc = ocol[rb];
+        if (oc >= 0) {
+          const double acc = acc0 + acc1;
+          if constexpr (ONEOUT) {
+            double y = alpha.s[0] * acc;
+            if (irow != nullptr) y = fma(beta.s[0], irow[oc], y);
+            orow[oc] = y;
+          } else {
+            const int o = oc >> 24, k = oc & 0xFFFFFF;
+            const double al = sel4(alpha.s[0], alpha.s[1], alpha.s[2], alpha.s[3], o);
+            const double be = sel4(beta.s[0], beta.s[1], beta.s[2], beta.s[3], o);
+            const double* ip = sel4(init.v[0].ptr, init.v[1].ptr, init.v[2].ptr, init.v[3].ptr, o);
+            const int64_t il = sel4(init.v[0].ld, init.v[1].ld, init.v[2].ld, init.v[3].ld, o);
+            const int ic = sel4(init.v[0].col0, init.v[1].col0, init.v[2].col0, init.v[3].col0, o);
+            double* op = sel4(out.v[0].ptr, out.v[1].ptr, out.v[2].ptr, out.v[3].ptr, o);
+            const int64_t ol = sel4(out.v[0].ld, out.v[1].ld, out.v[2].ld, out.v[3].ld, o);
+            const int occ = sel4(out.v[0].col0, out.v[1].col0, out.v[2].col0, out.v[3].col0, o);
+            double y = al * acc;
+            if (ip != nullptr) y += be * ip[(int64_t)row * il + ic + k];
+            op[(int64_t)row * ol + occ + k] = y;
+          }
+        }
+      }
+      bar_arrive_n(3 + cb, 512);  // done reading U buffer cb
+    }
+  }
+}
+
+template <int MAXOUT, bool ONEOUT>
+static int launch9ws(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
+                     const ViewSet& init, const ScalarSet& a, const ScalarSet& b, cudaStream_t st) {
+  const Smem9 L = smem9_ws_layout(pat.n_slices, prog);
+  static bool attr_set = false;
+  if (!attr_set) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, stencil9_ws_kernel<MAXOUT, ONEOUT>);
+    cudaFuncSetAttribute(stencil9_ws_kernel<MAXOUT, ONEOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         optin - (int)fa.sharedSizeBytes);
+    cudaGetLastError();
+    attr_set = true;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_ws_kernel<MAXOUT, ONEOUT>, 512, L.total);
+  if (occ < 1) return SGK_ELIMIT;
+  int64_t grid = (int64_t)sm_count() * occ;
+  if (grid > pat.n_rows) grid = pat.n_rows;
+  if (grid < 1) return SGK_OK;
+  stencil9_ws_kernel<MAXOUT, ONEOUT><<<(int)grid, 512, L.total, st>>>(pat, prog, in, out, init, a, b);
+  return check_launch("stencil9_ws_kernel");
+}
+
 template <int MAXOUT, bool RESIDENT, bool ONEOUT, bool BIG>
 static int launch9r(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
                     const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int threads, cudaStream_t st) {
@@ -422,6 +669,21 @@ static int launch9(const sgk_pattern9& pat, const sgk_program9& prog, const View
                    const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int n_out, int threads,
                    cudaStream_t st) {
   const bool res = prog.n_groups <= threads / 32;
+  // warp-specialised variant for product-heavy resident programs (6..8
+  // column groups: the config-4 matvec 1.34 -> 1.10 ms); programs with few
+  // groups keep the alternating kernel (their producers would idle: the
+  // config-5 level couplings measured 1.14 -> 1.22 ms).  SGKKT_S9_WS=0 / 1
+  // forces it off / on for every resident 8-warp program.
+  static const int ws_env = [] {
+    const char* v = getenv("SGKKT_S9_WS");
+    return v ? atoi(v) : -1;
+  }();
+  const bool ws = ws_env < 0 ? prog.n_groups >= 6 : ws_env != 0;
+  if (ws && res && threads == 256 && prog.n_groups <= 8) {
+    const int rc = n_out == 1 ? launch9ws<MAXOUT, true>(pat, prog, in, out, init, a, b, st)
+                              : launch9ws<MAXOUT, false>(pat, prog, in, out, init, a, b, st);
+    if (rc != SGK_ELIMIT) return rc;  // does not fit: the alternating kernel below
+  }
   if (threads > 256) {
     if (!res) {
       set_error("stencil9_kernel: more than 16 column groups need the 256-thread kernel");
