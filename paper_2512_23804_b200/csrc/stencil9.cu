@@ -486,12 +486,21 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
     }
     auto load_v = [&](int r) {
       const int32_t* cg = pat.colind9 + (int64_t)r * 9;
+      if (rncols == kGroupCols) {  // common case: immediate column offsets
+        const double* b = rvb + lane;
 #pragma unroll
-      for (int jj = 0; jj < 9; ++jj) {
-        const double* vr = rvb + (int64_t)__ldg(cg + jj) * rld;
+        for (int jj = 0; jj < 9; ++jj) {
+          const double* vr = b + (int64_t)__ldg(cg + jj) * rld;
 #pragma unroll
-        for (int c = 0; c < kCols; ++c)
-          rv[c][jj] = SGK_VLD(vr + (rncols == kGroupCols ? 32 * c + lane : min(32 * c + lane, rncols - 1)));
+          for (int c = 0; c < kCols; ++c) rv[c][jj] = SGK_VLD(vr + 32 * c);
+        }
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 9; ++jj) {
+          const double* vr = rvb + (int64_t)__ldg(cg + jj) * rld;
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) rv[c][jj] = SGK_VLD(vr + min(32 * c + lane, rncols - 1));
+        }
       }
     };
     int row = r_begin;
