@@ -36,6 +36,19 @@ def pytest_collection_modifyitems(config, items):
             item.add_marker(skip)
 
 
+@pytest.fixture(scope="session", autouse=True)
+def _built_library():
+    """A fresh checkout has no libsgkkt_b200.so (git-ignored): build it once
+    (nvcc cross-compiles without a GPU) so the ABI tests see the real file."""
+    from paper_2512_23804_b200 import _lib
+
+    if not _lib.library_path().exists():
+        import __graft_entry__
+
+        __graft_entry__.build()
+    yield
+
+
 @pytest.fixture
 def rng():
     return np.random.default_rng(SEED)
