@@ -56,6 +56,10 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int n_slices = pat.n_slices;
+  // single-chunk gather split (MAXOUT == 1): `parts` threads share a column;
+  // row-invariant, computed once (an integer division per phase otherwise)
+  const int parts = MAXOUT == 1 ? max(1, (int)blockDim.x / max(prog.n_out_cols, 1)) : 1;
+  const int part_col = threadIdx.x / parts, part_r = threadIdx.x - part_col * parts;
 
   for (int row = blockIdx.x; row < pat.n_rows; row += gridDim.x) {
     const int rs = __ldg(pat.rowptr + row);
@@ -118,15 +122,27 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
             const double* aa = abase + max(ta, 0) * len + c0;
             const double* ab = abase + max(tb, 0) * len + c0;
             double ua0 = 0.0, ua1 = 0.0, ub0 = 0.0, ub1 = 0.0;
+            if (cl == kChunk) {  // interior rows: no per-entry predicates (warp-uniform branch)
 #pragma unroll
-            for (int jj = 0; jj < kChunk; jj += 2) {
-              if (jj < cl) {
+              for (int jj = 0; jj < kChunk; jj += 2) {
                 ua0 = fma(aa[jj], v[jj], ua0);
                 ub0 = fma(ab[jj], v[jj], ub0);
+                if (jj + 1 < kChunk) {
+                  ua1 = fma(aa[jj + 1], v[jj + 1], ua1);
+                  ub1 = fma(ab[jj + 1], v[jj + 1], ub1);
+                }
               }
-              if (jj + 1 < cl) {
-                ua1 = fma(aa[jj + 1], v[jj + 1], ua1);
-                ub1 = fma(ab[jj + 1], v[jj + 1], ub1);
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < kChunk; jj += 2) {
+                if (jj < cl) {
+                  ua0 = fma(aa[jj], v[jj], ua0);
+                  ub0 = fma(ab[jj], v[jj], ub0);
+                }
+                if (jj + 1 < cl) {
+                  ua1 = fma(aa[jj + 1], v[jj + 1], ua1);
+                  ub1 = fma(ab[jj + 1], v[jj + 1], ub1);
+                }
               }
             }
             const int sa = (q - qbase) * 32 + lane;
@@ -155,8 +171,7 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
         // fewer output columns than threads: `parts` threads share a column,
         // thread part r takes entries r, r+parts, ... (coalesced table loads),
         // four independent accumulation chains per thread
-        const int parts = max(1, (int)blockDim.x / max(prog.n_out_cols, 1));
-        const int c = threadIdx.x / parts, r = threadIdx.x - c * parts;
+        const int c = part_col, r = part_r;
         if (c < prog.n_out_cols) {
           const int e0 = __ldg(gp + c), e1 = __ldg(gp + c + 1);
           double a0 = acc[0], a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -207,7 +222,6 @@ __global__ void __launch_bounds__(256) program_kernel(sgk_pattern pat, sgk_progr
     }
     if constexpr (MAXOUT == 1) {
       // combine the parts of each column in a fixed order (deterministic)
-      const int parts = max(1, (int)blockDim.x / max(prog.n_out_cols, 1));
       if (parts > 1) {
         ubuf[threadIdx.x] = acc[0];
         __syncthreads();
