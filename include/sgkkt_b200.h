@@ -285,7 +285,8 @@ int sgk_lognormal_fields(int64_t n_points, int32_t m, int32_t n_terms,
 
 /* One Chebyshev semi-iteration step on all columns (preconditioners.py:89-97):
  * x_new = omega*(scale .* (b - M x) + x - x_prev) + x_prev,
- * scale[i] = 1/(alpha*M_ii).  slice selects M inside the shared pattern.    */
+ * scale[i] = 1/(alpha*M_ii).  slice selects M inside the shared pattern.
+ * x and x_prev may be NULL: the zero iterate (first two steps from x0 = 0). */
 int sgk_cheb_step(const sgk_pattern* pat, int32_t slice, const double* scale,
                   int64_t n_cols, const double* b, const double* x,
                   const double* x_prev, double* x_new, double omega,

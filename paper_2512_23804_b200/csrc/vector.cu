@@ -9,24 +9,74 @@ constexpr int kRedBlocks = 148 * 8;  // fixed => reduction order is fixed
 
 // ---------------------------------------------------------------------------
 // K5: one step of chebyshev_mass_solve (preconditioners.py:89-97) over all
-// columns at once: thread per (row, column); the 9 mass coefficients of the
-// row are broadcast loads, the x rows are coalesced along the columns.
-__global__ void __launch_bounds__(256) cheb_step_kernel(sgk_pattern pat, int slice, const double* __restrict__ scale,
+// columns at once: one warp per mesh row (grid-stride), lanes along the
+// columns (coalesced x/b rows), two columns per lane per iteration so both
+// columns' neighbour loads are in flight together (the per-element kernel
+// was latency-bound at 1.7 TB/s).  x == nullptr / xp == nullptr stand for the zero
+// iterate (the first two steps start from x0 = 0: no reads of zero buffers).
+// The FMA order (row entries ascending from 0.0) is the per-element kernel's.
+constexpr int kChebRegs = 9;
+
+__device__ __forceinline__ double cheb_update(double omega, double si, double bv, double mx, double xv,
+                                              double xpv) {
+  return omega * (si * (bv - mx) + xv - xpv) + xpv;
+}
+
+__global__ void __launch_bounds__(256, 3) cheb_step_kernel(sgk_pattern pat, int slice, const double* __restrict__ scale,
                                  int64_t n_cols, const double* __restrict__ b,
                                  const double* __restrict__ x, const double* __restrict__ xp,
                                  double* __restrict__ xn, double omega) {
-  const int64_t total = (int64_t)pat.n_rows * n_cols;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(idx / n_cols);
-    const int64_t k = idx - (int64_t)i * n_cols;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool small = (int64_t)pat.n_rows * n_cols < ((int64_t)1 << 31);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < pat.n_rows; i += nw) {
     const int rs = __ldg(pat.rowptr + i), len = __ldg(pat.rowptr + i + 1) - rs;
     const double* a = pat.vals + (int64_t)rs * pat.n_slices + (int64_t)slice * len;
-    double mx = 0.0;
-    for (int jj = 0; jj < len; ++jj) mx = fma(__ldg(a + jj), __ldg(x + (int64_t)__ldg(pat.colind + rs + jj) * n_cols + k), mx);
-    const double resid = __ldg(b + idx) - mx;
-    const double xpv = xp ? __ldg(xp + idx) : 0.0;
-    xn[idx] = omega * (__ldg(scale + i) * resid + __ldg(x + idx) - xpv) + xpv;
+    const double si = __ldg(scale + i);
+    const int64_t row0 = i * n_cols;
+    if (len <= kChebRegs && small) {
+      // element offsets of the neighbour rows of x (< 2^31) in registers; the
+      // coefficients are warp-uniform L1 loads (registers go to the x values)
+      int off[kChebRegs];
+#pragma unroll
+      for (int jj = 0; jj < kChebRegs; ++jj) off[jj] = jj < len ? __ldg(pat.colind + rs + jj) * (int)n_cols : 0;
+      // two columns per lane per iteration: both columns' loads in flight
+      for (int64_t k = lane; k < n_cols; k += 64) {
+        const bool two = k + 32 < n_cols;
+        double m0 = 0.0, m1 = 0.0;
+        if (x != nullptr) {
+          double x0[kChebRegs], x1[kChebRegs];
+#pragma unroll
+          for (int jj = 0; jj < kChebRegs; ++jj) {
+            x0[jj] = jj < len ? __ldg(x + off[jj] + k) : 0.0;
+            x1[jj] = (jj < len && two) ? __ldg(x + off[jj] + k + 32) : 0.0;
+          }
+#pragma unroll
+          for (int jj = 0; jj < kChebRegs; ++jj)
+            if (jj < len) {
+              const double aj = __ldg(a + jj);
+              m0 = fma(aj, x0[jj], m0);
+              m1 = fma(aj, x1[jj], m1);
+            }
+        }
+        const int64_t e = row0 + k;
+        const double b0 = __ldg(b + e), b1 = two ? __ldg(b + e + 32) : 0.0;
+        const double xv0 = x ? __ldg(x + e) : 0.0, xv1 = (x && two) ? __ldg(x + e + 32) : 0.0;
+        const double xp0 = xp ? __ldg(xp + e) : 0.0, xp1 = (xp && two) ? __ldg(xp + e + 32) : 0.0;
+        xn[e] = cheb_update(omega, si, b0, m0, xv0, xp0);
+        if (two) xn[e + 32] = cheb_update(omega, si, b1, m1, xv1, xp1);
+      }
+    } else {
+      for (int64_t k = lane; k < n_cols; k += 32) {
+        double mx = 0.0;
+        if (x != nullptr)
+          for (int jj = 0; jj < len; ++jj)
+            mx = fma(__ldg(a + jj), __ldg(x + (int64_t)__ldg(pat.colind + rs + jj) * n_cols + k), mx);
+        const double xv = x ? __ldg(x + row0 + k) : 0.0;
+        const double xpv = xp ? __ldg(xp + row0 + k) : 0.0;
+        xn[row0 + k] = cheb_update(omega, si, __ldg(b + row0 + k), mx, xv, xpv);
+      }
+    }
   }
 }
 
@@ -173,13 +223,16 @@ using namespace sgk;
 extern "C" int sgk_cheb_step(const sgk_pattern* pat, int32_t slice, const double* scale,
                              int64_t n_cols, const double* b, const double* x, const double* x_prev,
                              double* x_new, double omega, void* stream) {
-  SGK_REQUIRE(pat && scale && b && x && x_new, "sgk_cheb_step: null argument");
+  SGK_REQUIRE(pat && scale && b && x_new, "sgk_cheb_step: null argument");
   SGK_REQUIRE(slice >= 0 && slice < pat->n_slices, "sgk_cheb_step: slice out of range");
   SGK_REQUIRE(x_new != x && x_new != x_prev, "sgk_cheb_step: x_new must not alias x/x_prev");
   const int64_t total = (int64_t)pat->n_rows * n_cols;
   if (total == 0) return SGK_OK;
-  cheb_step_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(*pat, slice, scale, n_cols, b, x,
-                                                                           x_prev, x_new, omega);
+  // one warp per row, 8 rows per CTA, grid = the resident CTAs (3 per SM)
+  int64_t blocks = ((int64_t)pat->n_rows + 7) / 8;
+  if (blocks > (int64_t)sm_count() * 3) blocks = (int64_t)sm_count() * 3;
+  cheb_step_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(*pat, slice, scale, n_cols, b, x, x_prev,
+                                                                   x_new, omega);
   return check_launch("cheb_step_kernel");
 }
 

@@ -102,18 +102,21 @@ class _DeviceMass:
         if not b2.is_contiguous():
             b2 = b2.contiguous()
         n_cols = b2.shape[1]
-        x_prev = torch.zeros_like(b2)
-        x = torch.zeros_like(b2)
+        # x0 = x_{-1} = 0: passed as NULL (the kernel reads no zero buffers)
+        x_prev = x = None
         lib = _lib.lib()
         stream = _lib.stream_ptr()
         for omega in _cheb_omegas(its):
             x_new = torch.empty_like(b2)
             rc = lib.sgk_cheb_step(
                 self.pattern.struct, self.slice, self.scale.data_ptr(), n_cols, b2.data_ptr(),
-                x.data_ptr(), x_prev.data_ptr(), x_new.data_ptr(), omega, stream,
+                None if x is None else x.data_ptr(), None if x_prev is None else x_prev.data_ptr(),
+                x_new.data_ptr(), omega, stream,
             )
             _lib.check(rc, "sgk_cheb_step")
             x_prev, x = x, x_new
+        if x is None:  # its == 0
+            x = torch.zeros_like(b2)
         return x.reshape(b.shape)
 
 
