@@ -314,6 +314,11 @@ int sgk_reduce_partials(const double* part, int32_t k, double* out,
 int sgk_axpby_dev(int64_t n, double sa, const double* da, int32_t inv_a,
                   const double* x, double sb, const double* db, double* y,
                   void* stream);
+/* out = s*((x0 + c1*x1) + c2*x2) in one pass, rounded exactly like the
+ * sgk_axpby_dev chain y=x0; y+=c1*x1; y+=c2*x2; y*=s (x1/x2 may be NULL;
+ * out may alias x0, not x1/x2).  MINRES three-term recurrences. */
+int sgk_lincomb3(int64_t n, const double* x0, double c1, const double* x1,
+                 double c2, const double* x2, double s, double* out, void* stream);
 /* Modified Gram–Schmidt step fused with the next inner product:
  * w -= h * q_i  (h = *dh), then partial dot of q_next with the new w.        */
 int sgk_mgs_step(int64_t n, const double* dh, const double* q_i, double* w,

@@ -151,6 +151,7 @@ _SIGNATURES = {
     "sgk_reduce_partials": (c_i32, [c_vp, c_i32, c_vp, c_i32, c_vp]),
     "sgk_axpby_dev": (c_i32, [c_i64, c_dbl, c_vp, c_i32, c_vp, c_dbl, c_vp, c_vp, c_vp]),
     "sgk_mgs_step": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "sgk_lincomb3": (c_i32, [c_i64, c_vp, c_dbl, c_vp, c_dbl, c_vp, c_dbl, c_vp, c_vp]),
     "sgk_f2n": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp]),
     "sgk_n2f": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp]),
     "sgk_last_error": (ctypes.c_char_p, []),

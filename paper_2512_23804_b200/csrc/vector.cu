@@ -164,6 +164,26 @@ __global__ void axpby_kernel(int64_t n, double sa, const double* da, int inv_a, 
   }
 }
 
+// out = s * ((x0 + c1 x1) + c2 x2), each step rounded exactly as the axpby
+// chain it replaces (y <- a x + b y with b = 1, then a final scale): one pass
+// instead of a copy + three axpby passes (the MINRES three-term recurrences).
+__device__ __forceinline__ double axpby_op(double a, double x, double b, double y) {
+  const double yi = (b == 0.0) ? 0.0 : b * y;
+  return (a == 0.0) ? yi : fma(a, x, yi);
+}
+
+__global__ void lincomb3_kernel(int64_t n, const double* x0, double c1, const double* __restrict__ x1, double c2,
+                                const double* __restrict__ x2, double s, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double t = x0[i];
+    if (x1) t = axpby_op(c1, __ldg(x1 + i), 1.0, t);
+    if (x2) t = axpby_op(c2, __ldg(x2 + i), 1.0, t);
+    if (s != 1.0) t = axpby_op(0.0, 0.0, s, t);
+    out[i] = t;
+  }
+}
+
 // Modified Gram–Schmidt step (krylov.py:81-84) fused with the partial dot
 // product of the next basis vector against the updated w.
 __global__ void __launch_bounds__(kRedThreads) mgs_step_kernel(int64_t n, const double* dh,
@@ -276,6 +296,15 @@ extern "C" int sgk_axpby_dev(int64_t n, double sa, const double* da, int32_t inv
   if (n == 0) return SGK_OK;
   axpby_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, sa, da, inv_a, x, sb, db, y);
   return check_launch("axpby_kernel");
+}
+
+extern "C" int sgk_lincomb3(int64_t n, const double* x0, double c1, const double* x1, double c2,
+                            const double* x2, double s, double* out, void* stream) {
+  SGK_REQUIRE(x0 && out, "sgk_lincomb3: null argument");
+  SGK_REQUIRE(out == x0 || (out != x1 && out != x2), "sgk_lincomb3: out may alias x0 only");
+  if (n == 0) return SGK_OK;
+  lincomb3_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, x0, c1, x1, c2, x2, s, out);
+  return check_launch("lincomb3_kernel");
 }
 
 extern "C" int sgk_mgs_step(int64_t n, const double* dh, const double* q_i, double* w,

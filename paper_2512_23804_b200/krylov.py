@@ -32,7 +32,7 @@ import numpy as np
 import torch
 
 from .device import as_device_state, device
-from .vec import Reducer, axpby
+from .vec import Reducer, axpby, lincomb3
 
 __all__ = ["FgmresConfig", "KrylovConfig", "SolveReport", "cg", "fgmres", "minres"]
 
@@ -283,16 +283,14 @@ def minres(apply_op: Callable, apply_prec: Callable | None, b, cfg: FgmresConfig
     it = 0
     max_iters = cfg.max_iters
     for it in range(1, max_iters + 1):
-        zn = z.clone() if z.data_ptr() in (v.data_ptr(), r.data_ptr()) else z
-        axpby(zn, None, 0.0, 1.0 / gamma)  # z_j /= gamma_j
+        zn = torch.empty_like(z) if z.data_ptr() in (v.data_ptr(), r.data_ptr()) else z
+        lincomb3(zn, z, s=1.0 / gamma)  # z_j /= gamma_j
         az = _call(apply_op, zn)
         if az.data_ptr() == zn.data_ptr():
             az = az.clone()
         delta = float(red.dot(az, zn, sc[1:2]).item())
         # v_{j+1} = A z_j - (delta/gamma) v_j - (gamma/gamma_old) v_{j-1}
-        v_new = az.clone()
-        axpby(v_new, v, -delta / gamma, 1.0)
-        axpby(v_new, v_old, -gamma / gamma_old, 1.0)
+        v_new = lincomb3(torch.empty_like(az), az, -delta / gamma, v, -gamma / gamma_old, v_old)
         z_new = _call(prec, v_new)
         zv = float(red.dot(z_new, v_new, sc[2:3]).item())
         if zv < 0.0:
@@ -305,14 +303,9 @@ def minres(apply_op: Callable, apply_prec: Callable | None, b, cfg: FgmresConfig
         c_new = a0 / a1
         s_new = gamma_new / a1
         # w_{j+1} = (z_j - a3 w_{j-1} - a2 w_j)/a1 ; same recurrence for A w
-        w_new = zn.clone()
-        axpby(w_new, w_old, -a3, 1.0)
-        axpby(w_new, w, -a2, 1.0)
-        axpby(w_new, None, 0.0, 1.0 / a1)
-        aw_new = az.clone()
-        axpby(aw_new, aw_old, -a3, 1.0)
-        axpby(aw_new, aw, -a2, 1.0)
-        axpby(aw_new, None, 0.0, 1.0 / a1)
+        # (one fused pass each, rounded exactly like the axpby chains)
+        w_new = lincomb3(torch.empty_like(zn), zn, -a3, w_old, -a2, w, 1.0 / a1)
+        aw_new = lincomb3(torch.empty_like(az), az, -a3, aw_old, -a2, aw, 1.0 / a1)
         axpby(x, w_new, c_new * eta, 1.0)
         axpby(r, aw_new, -c_new * eta, 1.0)
         eta = -s_new * eta

@@ -7,7 +7,7 @@ import torch
 
 from . import _lib
 
-__all__ = ["Reducer", "axpby", "colscale"]
+__all__ = ["Reducer", "axpby", "colscale", "lincomb3"]
 
 
 class Reducer:
@@ -65,6 +65,18 @@ def axpby(y: torch.Tensor, x: torch.Tensor | None, a: float = 1.0, b: float = 1.
                                  db.data_ptr() if db is not None else None, y.data_ptr(), _lib.stream_ptr()),
                "sgk_axpby_dev")
     return y
+
+
+def lincomb3(out: torch.Tensor, x0: torch.Tensor, c1: float = 0.0, x1: torch.Tensor | None = None,
+             c2: float = 0.0, x2: torch.Tensor | None = None, s: float = 1.0) -> torch.Tensor:
+    """out <- s*((x0 + c1 x1) + c2 x2), bit-identical to the axpby chain
+    (out = x0.clone(); axpby(out, x1, c1); axpby(out, x2, c2); axpby(out, None, 0, s))
+    in one pass; `out` may be `x0`."""
+    lib = _lib.lib()
+    _lib.check(lib.sgk_lincomb3(out.numel(), x0.data_ptr(), c1, x1.data_ptr() if x1 is not None else None, c2,
+                                x2.data_ptr() if x2 is not None else None, s, out.data_ptr(), _lib.stream_ptr()),
+               "sgk_lincomb3")
+    return out
 
 
 def colscale(x: torch.Tensor, w: torch.Tensor | None, s: float, out: torch.Tensor, invert: bool = False):

@@ -124,3 +124,26 @@ def test_krylov_argument_errors_and_caps():
     # max_iters is capped by the problem size (krylov.py:61)
     x, rep = fgmres(op, None, b, FgmresConfig(tol=1e-15, max_iters=500))
     assert rep.iterations <= n
+
+
+@pytest.mark.parametrize("c1,c2,s", [(-0.37, 1.25, 1.0 / 3.0), (0.0, -2.0, 1.0), (-0.0, 0.0, 0.5), (1.5, 0.0, 1.0)])
+def test_lincomb3_matches_the_axpby_chain_bitwise(c1, c2, s):
+    """The fused MINRES recurrence pass rounds exactly like the axpby chain it
+    replaced (zero coefficients skipped the same way; out aliasing x0)."""
+    import torch
+
+    from paper_2512_23804_b200.vec import axpby, lincomb3
+
+    g = torch.Generator().manual_seed(5)
+    x0, x1, x2 = (torch.randn(100_003, generator=g, dtype=torch.float64).cuda() for _ in range(3))
+    want = x0.clone()
+    axpby(want, x1, c1, 1.0)
+    axpby(want, x2, c2, 1.0)
+    axpby(want, None, 0.0, s)
+    got = lincomb3(torch.empty_like(x0), x0, c1, x1, c2, x2, s)
+    assert torch.equal(got, want)
+    inplace = x0.clone()
+    lincomb3(inplace, inplace, c1, x1, c2, x2, s)
+    assert torch.equal(inplace, want)
+    with pytest.raises(Exception):
+        lincomb3(x1, x0, c1, x1, c2, x2, s)
