@@ -187,11 +187,20 @@ def _load():
     return handle
 
 
+_DEVICE_OK = False
+
+
 def lib():
-    """The loaded library; requires a visible CUDA device (no CPU fallback)."""
+    """The loaded library; requires a visible CUDA device (no CPU fallback).
+    The device check runs until it first succeeds (a device cannot vanish
+    from a running process; this is on every launch's host path)."""
+    global _DEVICE_OK
+    if _DEVICE_OK and _LIB is not None:
+        return _LIB
     handle = _load()
     if not torch.cuda.is_available():
         raise RuntimeError("libsgkkt_b200 needs a CUDA device; none is visible (no CPU fallback)")
+    _DEVICE_OK = True
     return handle
 
 
@@ -209,8 +218,12 @@ def check(rc: int, what: str) -> None:
 
 
 def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    """cudaStream_t of `stream`, else of torch's current stream on the current
+    device (the raw-pointer query skips torch.cuda.current_stream()'s Python
+    wrapper: ~15 us per call, paid on every launch)."""
+    if stream is not None:
+        return int(stream.cuda_stream)
+    return int(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 def launch_count() -> int:
