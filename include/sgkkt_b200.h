@@ -291,6 +291,14 @@ int sgk_cheb_step(const sgk_pattern* pat, int32_t slice, const double* scale,
                   int64_t n_cols, const double* b, const double* x,
                   const double* x_prev, double* x_new, double omega,
                   void* stream);
+/* The same step on n_batch independent blocks stored back to back
+ * (block bi at offset bi*n_rows*n_cols of b/x/x_prev/x_new): the N_t mass
+ * solves of the time-dependent preconditioner (preconditioners.py:278-312)
+ * in one launch per step. */
+int sgk_cheb_step_batched(const sgk_pattern* pat, int32_t slice, const double* scale,
+                          int64_t n_batch, int64_t n_cols, const double* b,
+                          const double* x, const double* x_prev, double* x_new,
+                          double omega, void* stream);
 
 /* y[i,k] = s * x[i,k] * w[k]  (w may be NULL: y = s*x).                   */
 int sgk_colscale(int64_t n_rows, int64_t n_cols, const double* x,

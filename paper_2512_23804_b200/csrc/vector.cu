@@ -23,13 +23,21 @@ __device__ __forceinline__ double cheb_update(double omega, double si, double bv
 }
 
 __global__ void __launch_bounds__(256, 3) cheb_step_kernel(sgk_pattern pat, int slice, const double* __restrict__ scale,
-                                 int64_t n_cols, const double* __restrict__ b,
-                                 const double* __restrict__ x, const double* __restrict__ xp,
-                                 double* __restrict__ xn, double omega) {
+                                 int64_t n_batch, int64_t n_cols, const double* __restrict__ b_all,
+                                 const double* __restrict__ x_all, const double* __restrict__ xp_all,
+                                 double* __restrict__ xn_all, double omega) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const bool small = (int64_t)pat.n_rows * n_cols < ((int64_t)1 << 31);
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < pat.n_rows; i += nw) {
+  const int64_t n_items = n_batch * pat.n_rows;
+  for (int64_t gi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gi < n_items; gi += nw) {
+    // batch bi: an independent (n_rows x n_cols) block at offset bi*n_rows*n_cols
+    const int64_t bi = gi / pat.n_rows, i = gi - bi * pat.n_rows;
+    const int64_t base = bi * pat.n_rows * n_cols;
+    const double* b = b_all + base;
+    const double* x = x_all ? x_all + base : nullptr;
+    const double* xp = xp_all ? xp_all + base : nullptr;
+    double* xn = xn_all + base;
     const int rs = __ldg(pat.rowptr + i), len = __ldg(pat.rowptr + i + 1) - rs;
     const double* a = pat.vals + (int64_t)rs * pat.n_slices + (int64_t)slice * len;
     const double si = __ldg(scale + i);
@@ -240,20 +248,27 @@ static int transpose(int64_t rows, int64_t cols, const double* in, double* out, 
 
 using namespace sgk;
 
+extern "C" int sgk_cheb_step_batched(const sgk_pattern* pat, int32_t slice, const double* scale, int64_t n_batch,
+                                     int64_t n_cols, const double* b, const double* x, const double* x_prev,
+                                     double* x_new, double omega, void* stream) {
+  SGK_REQUIRE(pat && scale && b && x_new, "sgk_cheb_step: null argument");
+  SGK_REQUIRE(slice >= 0 && slice < pat->n_slices, "sgk_cheb_step: slice out of range");
+  SGK_REQUIRE(n_batch >= 0 && n_cols >= 0, "sgk_cheb_step: negative size");
+  SGK_REQUIRE(x_new != x && x_new != x_prev, "sgk_cheb_step: x_new must not alias x/x_prev");
+  const int64_t rows = n_batch * pat->n_rows;
+  if (rows == 0 || n_cols == 0) return SGK_OK;
+  // one warp per row, 8 rows per CTA, grid = the resident CTAs (3 per SM)
+  int64_t blocks = (rows + 7) / 8;
+  if (blocks > (int64_t)sm_count() * 3) blocks = (int64_t)sm_count() * 3;
+  cheb_step_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(*pat, slice, scale, n_batch, n_cols, b, x,
+                                                                   x_prev, x_new, omega);
+  return check_launch("cheb_step_kernel");
+}
+
 extern "C" int sgk_cheb_step(const sgk_pattern* pat, int32_t slice, const double* scale,
                              int64_t n_cols, const double* b, const double* x, const double* x_prev,
                              double* x_new, double omega, void* stream) {
-  SGK_REQUIRE(pat && scale && b && x_new, "sgk_cheb_step: null argument");
-  SGK_REQUIRE(slice >= 0 && slice < pat->n_slices, "sgk_cheb_step: slice out of range");
-  SGK_REQUIRE(x_new != x && x_new != x_prev, "sgk_cheb_step: x_new must not alias x/x_prev");
-  const int64_t total = (int64_t)pat->n_rows * n_cols;
-  if (total == 0) return SGK_OK;
-  // one warp per row, 8 rows per CTA, grid = the resident CTAs (3 per SM)
-  int64_t blocks = ((int64_t)pat->n_rows + 7) / 8;
-  if (blocks > (int64_t)sm_count() * 3) blocks = (int64_t)sm_count() * 3;
-  cheb_step_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(*pat, slice, scale, n_cols, b, x, x_prev,
-                                                                   x_new, omega);
-  return check_launch("cheb_step_kernel");
+  return sgk_cheb_step_batched(pat, slice, scale, 1, n_cols, b, x, x_prev, x_new, omega, stream);
 }
 
 extern "C" int sgk_colscale(int64_t n_rows, int64_t n_cols, const double* x, const double* w,

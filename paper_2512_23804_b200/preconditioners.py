@@ -99,17 +99,27 @@ class _DeviceMass:
 
     def cheb(self, b: torch.Tensor, its: int) -> torch.Tensor:
         b2 = b.reshape(b.shape[0], -1)
+        return self._run(b2, 1, b2.shape[1], its).reshape(b.shape)
+
+    def cheb_batched(self, b: torch.Tensor, its: int) -> torch.Tensor:
+        """chebyshev_mass_solve on each (N, n_cols) block of a (n_b, N, n_cols)
+        stack in one launch per step (the time steps of the PINT
+        preconditioner); each block's result equals `cheb` on it bitwise."""
+        if b.dim() != 3:
+            raise ValueError("expected a (n_blocks, N, n_cols) stack")
+        return self._run(b, b.shape[0], b.shape[2], its)
+
+    def _run(self, b2: torch.Tensor, n_batch: int, n_cols: int, its: int) -> torch.Tensor:
         if not b2.is_contiguous():
             b2 = b2.contiguous()
-        n_cols = b2.shape[1]
         # x0 = x_{-1} = 0: passed as NULL (the kernel reads no zero buffers)
         x_prev = x = None
         lib = _lib.lib()
         stream = _lib.stream_ptr()
         for omega in _cheb_omegas(its):
             x_new = torch.empty_like(b2)
-            rc = lib.sgk_cheb_step(
-                self.pattern.struct, self.slice, self.scale.data_ptr(), n_cols, b2.data_ptr(),
+            rc = lib.sgk_cheb_step_batched(
+                self.pattern.struct, self.slice, self.scale.data_ptr(), n_batch, n_cols, b2.data_ptr(),
                 None if x is None else x.data_ptr(), None if x_prev is None else x_prev.data_ptr(),
                 x_new.data_ptr(), omega, stream,
             )
@@ -117,7 +127,7 @@ class _DeviceMass:
             x_prev, x = x, x_new
         if x is None:  # its == 0
             x = torch.zeros_like(b2)
-        return x.reshape(b.shape)
+        return x
 
 
 # device copies of mass matrices used by chebyshev_mass_solve, keyed by the

@@ -283,10 +283,20 @@ class TimeKKTPreconditioner:
         g = _blocks(sys, r)
         o = _blocks(sys, out)
         wv = self._weights()
-        for k in (range(sys.n_t) if step_order is None else step_order):
+        steps = list(range(sys.n_t) if step_order is None else step_order)
+        dm = getattr(self.mass_solve, "device_mass", None)
+        if dm is not None:
+            # the time steps' y and u mass solves are independent: one batched
+            # Chebyshev launch per step over all 2 N_t blocks
+            its = self.mass_solve.its
+            mass_yu = dm.cheb_batched(g[0:2].reshape(2 * sys.n_t, st.n_h, st.n_xi), its).view(
+                2, sys.n_t, st.n_h, st.n_xi)
+        for k in steps:
             dk = float(wsteps[k])
-            colscale(self._mass(g[0, k]), wv, 1.0 / (tau * dk), o[0, k], invert=True)
-            colscale(self._mass(g[1, k]), None, 1.0 / (st.beta * tau * dk), o[1, k])
+            my = mass_yu[0, k] if dm is not None else self._mass(g[0, k])
+            mu = mass_yu[1, k] if dm is not None else self._mass(g[1, k])
+            colscale(my, wv, 1.0 / (tau * dk), o[0, k], invert=True)
+            colscale(mu, None, 1.0 / (st.beta * tau * dk), o[1, k])
             z1 = _richardson_device(self.z_operator, self.sweep, g[2, k], self.richardson_steps)
             ww = torch.empty_like(z1)
             run_program(st.pattern, self._weighted_mass(dk), [(z1, 0)], [(ww, 0)], alpha=[1.0], beta=[0.0])

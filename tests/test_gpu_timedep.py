@@ -92,3 +92,24 @@ def test_pint_with_fastdiag_leads_matches_reference():
     assert rep.converged and abs(rep.iterations - int(c["fgmres_iters"])) <= 1
     xf = from_device_layout(sys_, x)
     assert np.linalg.norm(xf - c["fgmres_x"]) <= 1e-8 * np.linalg.norm(c["fgmres_x"])
+
+
+def test_batched_mass_solves_equal_per_block_solves():
+    """The PINT preconditioner's batched Chebyshev mass solve (all 2 N_t
+    blocks per launch) equals the per-block solve bitwise, including a block
+    count above the grid's resident warps and a zero-step solve."""
+    import torch
+
+    from paper_2512_23804_b200.preconditioners import make_mass_solver
+    from paper_2512_23804_b200.problems import build_problem, steady_system
+
+    b = build_problem(2)
+    st = steady_system(b)
+    ms = make_mass_solver(st.mass, "cheb5", st.pattern, st.mass_slice)
+    dm = ms.device_mass
+    g = torch.Generator().manual_seed(3)
+    stack = torch.randn((5, st.n_h, st.n_xi), generator=g, dtype=torch.float64).cuda()
+    for its in (5, 1, 0):
+        got = dm.cheb_batched(stack, its)
+        for i in range(stack.shape[0]):
+            assert torch.equal(got[i], dm.cheb(stack[i], its)), (its, i)
