@@ -276,13 +276,64 @@ class TimeKKTPreconditioner:
         out = self.mass_solve(b)
         return out if isinstance(out, torch.Tensor) and out.is_cuda else as_device_state(out)[0]
 
+    def _stepwise_schur(self):
+        """The lambda block's Z^-1 M_gamma Z^-1 for all N_t steps at once.
+
+        Step k's (N, n_xi) block becomes columns l*N_t + k of one
+        (N, n_xi*N_t) matrix (a transpose of the (N_t, N*n_xi) stack), so the
+        steps' hGS sweeps are ONE sweep with couplings H_t (x) I_{N_t} and
+        level boundaries scaled by N_t: every level solve and coupling
+        launch covers all steps (the same per-column arithmetic as the
+        per-step loop; the gather may sum in a different order)."""
+        bt = self._cache.get("stepwise")
+        if bt is None:
+            sys = self.system
+            st = sys.steady
+            n_t, n_xi = sys.n_t, st.n_xi
+            eye = sp.identity(n_t, format="csr")
+            op = self.z_operator
+            op_x = KroneckerSumOperator(couplings=[sp.kron(h, eye, format="csr") for h in op.couplings],
+                                        operators=list(op.operators))
+            op_x._cache["pattern"] = op.pattern  # same A_t: share the device values
+            part_x = LevelPartition(boundaries=np.asarray(self.sweep.partition.boundaries, np.int64) * n_t)
+            sweep_x = HierarchicalGaussSeidel(operator=op_x, partition=part_x, n_tau=self.sweep.n_tau,
+                                              lead_factor=self.sweep.lead_factor)
+            # weighted mass of step k: dk * M Z H_gamma -> H_gamma (x) diag(d)
+            wm = sp.kron(st.triple.objective_weight.tocsr(), sp.diags(np.asarray(sys.stencil.weights, np.float64)),
+                         format="csr")
+            cp = coupling_from_csr(0, 0, st.mass_slice, wm, (0, n_xi * n_t), (0, n_xi * n_t), 1.0)
+            bt = (op_x, sweep_x, DeviceProgram([cp], (n_xi * n_t,), n_inputs=1))
+            self._cache["stepwise"] = bt
+        return bt
+
+    def _schur_all_steps(self, r_lam: torch.Tensor, o_lam: torch.Tensor) -> None:
+        from . import _lib
+
+        sys = self.system
+        st = sys.steady
+        n_t, n_cells = sys.n_t, st.n_h * st.n_xi
+        op_x, sweep_x, wm = self._stepwise_schur()
+        lib = _lib.lib()
+        zin = torch.empty((st.n_h, st.n_xi * n_t), dtype=torch.float64, device=r_lam.device)
+        # (N_t, N*n_xi) row-major -> (N*n_xi, N_t): column l*N_t + k of zin is step k's column l
+        _lib.check(lib.sgk_n2f(n_t, n_cells, r_lam.data_ptr(), zin.data_ptr(), _lib.stream_ptr()), "sgk_n2f")
+        z1 = _richardson_device(op_x, sweep_x, zin, self.richardson_steps)
+        ww = torch.empty_like(z1)
+        run_program(st.pattern, wm, [(z1, 0)], [(ww, 0)], alpha=[1.0], beta=[0.0])
+        z2 = _richardson_device(op_x, sweep_x, ww, self.richardson_steps)
+        colscale(z2, None, sys.tau, z2)
+        _lib.check(lib.sgk_n2f(n_cells, n_t, z2.data_ptr(), o_lam.data_ptr(), _lib.stream_ptr()), "sgk_n2f")
+
     def apply_device(self, r: torch.Tensor, out: torch.Tensor, step_order: Sequence[int] | None = None):
+        """All steps batched (default), or the per-step loop in `step_order`
+        (the reference's structure; block diagonal in time, so any order)."""
         sys = self.system
         st = sys.steady
         tau, wsteps = sys.tau, sys.stencil.weights
         g = _blocks(sys, r)
         o = _blocks(sys, out)
         wv = self._weights()
+        batched = step_order is None
         steps = list(range(sys.n_t) if step_order is None else step_order)
         dm = getattr(self.mass_solve, "device_mass", None)
         if dm is not None:
@@ -297,11 +348,15 @@ class TimeKKTPreconditioner:
             mu = mass_yu[1, k] if dm is not None else self._mass(g[1, k])
             colscale(my, wv, 1.0 / (tau * dk), o[0, k], invert=True)
             colscale(mu, None, 1.0 / (st.beta * tau * dk), o[1, k])
+            if batched:
+                continue
             z1 = _richardson_device(self.z_operator, self.sweep, g[2, k], self.richardson_steps)
             ww = torch.empty_like(z1)
             run_program(st.pattern, self._weighted_mass(dk), [(z1, 0)], [(ww, 0)], alpha=[1.0], beta=[0.0])
             z2 = _richardson_device(self.z_operator, self.sweep, ww, self.richardson_steps)
             colscale(z2, None, tau, o[2, k])
+        if batched:
+            self._schur_all_steps(g[2], o[2])
         return out
 
     def apply(self, r, step_order: Sequence[int] | None = None):

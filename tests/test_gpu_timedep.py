@@ -49,8 +49,13 @@ def test_pint_preconditioner(which):
     prec = build_time_preconditioner(sys_, part, mass_solver="cheb5", n_tau=n_tau)
     got = prec.apply(c["v"])
     assert _rel(got, c[f"pint_tau{n_tau}"]) <= 1e-12
-    # block diagonal in time: step order is irrelevant, bit for bit
-    assert np.array_equal(prec.apply(c["v"], step_order=[2, 0, 3, 1]), got)
+    # block diagonal in time: in the per-step loop the step order is
+    # irrelevant, bit for bit; the default all-steps-batched path agrees with
+    # it to rounding
+    inorder = prec.apply(c["v"], step_order=list(range(sys_.n_t)))
+    assert np.array_equal(prec.apply(c["v"], step_order=[2, 0, 3, 1]), inorder)
+    assert _rel(inorder, c[f"pint_tau{n_tau}"]) <= 1e-12
+    assert _rel(got, inorder) <= 1e-13
 
 
 def test_pint_fgmres_solve_matches_reference():
@@ -113,3 +118,19 @@ def test_batched_mass_solves_equal_per_block_solves():
         got = dm.cheb_batched(stack, its)
         for i in range(stack.shape[0]):
             assert torch.equal(got[i], dm.cheb(stack[i], its)), (its, i)
+
+
+@pytest.mark.parametrize("lead", ["lu", "fastdiag"])
+def test_step_batched_schur_block_matches_per_step_loop(lead):
+    """All N_t steps' Z^-1 M_gamma Z^-1 as one sweep over interleaved step
+    columns (couplings H_t (x) I_{N_t}) against the reference-shaped per-step
+    loop: y and u blocks bitwise, the lambda block to rounding."""
+    from paper_2512_23804_b200.timedep import build_time_preconditioner
+
+    c, sys_, part = _system()
+    prec = build_time_preconditioner(sys_, part, mass_solver="cheb5", n_tau=int(c["n_terms"]), lead_solver=lead)
+    batched = prec.apply(c["v"])
+    stepwise = prec.apply(c["v"], step_order=list(range(sys_.n_t)))
+    n = len(batched) // 3
+    assert np.array_equal(batched[:2 * n], stepwise[:2 * n])
+    assert _rel(batched[2 * n:], stepwise[2 * n:]) <= 1e-13
