@@ -658,7 +658,7 @@ def run_ours(args):
         if not args.no_solve_cfg5:
             solves["cfg5"] = solve_block(5, [1e-2, 1e-4, 1e-6])
             solves["cfg5_apply_breakdown"] = apply_breakdown(5)
-        if args.solve_time:
+        if not args.no_solve_time:
             solves["time_dependent"] = time_solve_block(args.time_cpu)
         line["solves"] = solves
     if rank == 0 and args.table_out:
@@ -687,7 +687,8 @@ def main():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--solve-cfg5", action="store_true", help="(default on; kept for compatibility)")
     ap.add_argument("--no-solve-cfg5", action="store_true", help="skip the cfg5 beta sweep")
-    ap.add_argument("--solve-time", action="store_true", help="time-dependent PINT solve (SURVEY 8(f) row 1)")
+    ap.add_argument("--solve-time", action="store_true", help="(default on; kept for compatibility)")
+    ap.add_argument("--no-solve-time", action="store_true", help="skip the time-dependent PINT solve (SURVEY 8(f) row 1)")
     ap.add_argument("--time-cpu", action="store_true", help="also time the CPU port of the time-dependent solve")
     ap.add_argument("--ref-budget", type=float, default=3.0)
     ap.add_argument("--table-out", default=None,
