@@ -19,7 +19,11 @@ M lambda_{k+1} and M y_{k-1}.  The PINT preconditioner is block diagonal in
 time: every step runs the Chebyshev mass solves and the Richardson-wrapped
 hGS sweep with the time-shifted lead term (1 + tau sqrt((1+gamma)/beta)) M +
 tau A_1, independently of the other steps (the step order never matters —
-reference tests/test_preconditioners.py:339-345).
+reference tests/test_preconditioners.py:339-345).  So the device path runs
+all steps at once: the 2 N_t mass solves as one batched Chebyshev launch per
+step, and the N_t Schur blocks as ONE sweep over an (N, n_xi*N_t) matrix with
+interleaved step columns (couplings H_t (x) I_{N_t}); `step_order=` keeps the
+reference's per-step loop.
 """
 
 from __future__ import annotations
