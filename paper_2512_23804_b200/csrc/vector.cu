@@ -22,7 +22,7 @@ __device__ __forceinline__ double cheb_update(double omega, double si, double bv
   return omega * (si * (bv - mx) + xv - xpv) + xpv;
 }
 
-__global__ void __launch_bounds__(256, 3) cheb_step_kernel(sgk_pattern pat, int slice, const double* __restrict__ scale,
+__global__ void __launch_bounds__(256, 4) cheb_step_kernel(sgk_pattern pat, int slice, const double* __restrict__ scale,
                                  int64_t n_batch, int64_t n_cols, const double* __restrict__ b_all,
                                  const double* __restrict__ x_all, const double* __restrict__ xp_all,
                                  double* __restrict__ xn_all, double omega) {
@@ -43,11 +43,10 @@ __global__ void __launch_bounds__(256, 3) cheb_step_kernel(sgk_pattern pat, int 
     const double si = __ldg(scale + i);
     const int64_t row0 = i * n_cols;
     if (len <= kChebRegs && small) {
-      // element offsets of the neighbour rows of x (< 2^31) in registers; the
-      // coefficients are warp-uniform L1 loads (registers go to the x values)
-      int off[kChebRegs];
-#pragma unroll
-      for (int jj = 0; jj < kChebRegs; ++jj) off[jj] = jj < len ? __ldg(pat.colind + rs + jj) * (int)n_cols : 0;
+      // column indices and coefficients are warp-uniform L1 loads (registers
+      // go to the two columns' x values; 64 registers -> 4 CTAs per SM);
+      // element offsets fit in 32 bits here
+      const int32_t* ci = pat.colind + rs;
       // two columns per lane per iteration: both columns' loads in flight
       for (int64_t k = lane; k < n_cols; k += 64) {
         const bool two = k + 32 < n_cols;
@@ -56,8 +55,8 @@ __global__ void __launch_bounds__(256, 3) cheb_step_kernel(sgk_pattern pat, int 
           double x0[kChebRegs], x1[kChebRegs];
 #pragma unroll
           for (int jj = 0; jj < kChebRegs; ++jj) {
-            x0[jj] = jj < len ? __ldg(x + off[jj] + k) : 0.0;
-            x1[jj] = (jj < len && two) ? __ldg(x + off[jj] + k + 32) : 0.0;
+            x0[jj] = jj < len ? __ldg(x + __ldg(ci + jj) * (int)n_cols + k) : 0.0;
+            x1[jj] = (jj < len && two) ? __ldg(x + __ldg(ci + jj) * (int)n_cols + k + 32) : 0.0;
           }
 #pragma unroll
           for (int jj = 0; jj < kChebRegs; ++jj)
@@ -257,9 +256,9 @@ extern "C" int sgk_cheb_step_batched(const sgk_pattern* pat, int32_t slice, cons
   SGK_REQUIRE(x_new != x && x_new != x_prev, "sgk_cheb_step: x_new must not alias x/x_prev");
   const int64_t rows = n_batch * pat->n_rows;
   if (rows == 0 || n_cols == 0) return SGK_OK;
-  // one warp per row, 8 rows per CTA, grid = the resident CTAs (3 per SM)
+  // one warp per row, 8 rows per CTA, grid = the resident CTAs (4 per SM)
   int64_t blocks = (rows + 7) / 8;
-  if (blocks > (int64_t)sm_count() * 3) blocks = (int64_t)sm_count() * 3;
+  if (blocks > (int64_t)sm_count() * 4) blocks = (int64_t)sm_count() * 4;
   cheb_step_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(*pat, slice, scale, n_batch, n_cols, b, x,
                                                                    x_prev, x_new, omega);
   return check_launch("cheb_step_kernel");
