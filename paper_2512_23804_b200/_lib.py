@@ -225,7 +225,14 @@ def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
     wrapper: ~15 us per call, paid on every launch)."""
     if stream is not None:
         return int(stream.cuda_stream)
-    return int(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
+    if _RAW_STREAM is not None:
+        return int(_RAW_STREAM(torch._C._cuda_getDevice()))
+    return int(torch.cuda.current_stream().cuda_stream)
+
+
+# private torch entry point (present in the torch this image ships); the
+# public query above is the fallback
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None) if hasattr(torch._C, "_cuda_getDevice") else None
 
 
 def launch_count() -> int:
