@@ -147,3 +147,23 @@ def test_lincomb3_matches_the_axpby_chain_bitwise(c1, c2, s):
     assert torch.equal(inplace, want)
     with pytest.raises(Exception):
         lincomb3(x1, x0, c1, x1, c2, x2, s)
+
+
+def test_launches_follow_torchs_current_stream():
+    """The raw current-stream query used on every launch returns the stream a
+    `torch.cuda.stream(...)` context selected (launches are stream-ordered
+    with the caller's torch work)."""
+    import torch
+
+    from paper_2512_23804_b200 import _lib
+    from paper_2512_23804_b200.vec import lincomb3
+
+    side = torch.cuda.Stream()
+    assert _lib.stream_ptr() == torch.cuda.current_stream().cuda_stream
+    x = torch.arange(1000, dtype=torch.float64, device="cuda")
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        assert _lib.stream_ptr() == side.cuda_stream
+        y = lincomb3(torch.empty_like(x), x, s=2.0)
+    side.synchronize()
+    assert torch.equal(y, 2.0 * x)
