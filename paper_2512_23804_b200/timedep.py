@@ -12,10 +12,13 @@ lambda steps], each step an F-order vec of an (N, n_xi) block.  On the device
 the same vector is (3, N_t, N, n_xi) node-major blocks; NumPy inputs are
 converted at the boundary (`to_device_layout` / `from_device_layout`).
 
-Per step k the operator is one fused program launch over the shared pattern
-(the steady KKT program with the step's tau / trapezoid-weight factors folded
-into the gather coefficients) plus one launch for the time couplings
-M lambda_{k+1} and M y_{k-1}.  The PINT preconditioner is block diagonal in
+The operator (`time_kkt_apply`) is ONE fused program launch over the shared
+pattern on interleaved step columns (column l*N_t + k = step k's column l):
+the steady KKT couplings with each step's tau / trapezoid-weight factors as
+diagonal N_t x N_t factors, and the time couplings M lambda_{k+1} and
+M y_{k-1} as column shifts; a transpose per block on each side.
+`time_kkt_apply_device` keeps the per-step form (one program per step plus
+one launch for the time couplings).  The PINT preconditioner is block diagonal in
 time: every step runs the Chebyshev mass solves and the Richardson-wrapped
 hGS sweep with the time-shifted lead term (1 + tau sqrt((1+gamma)/beta)) M +
 tau A_1, independently of the other steps (the step order never matters —
@@ -54,6 +57,8 @@ __all__ = [
     "join_time_blocks",
     "split_time_blocks",
     "time_kkt_apply",
+    "time_kkt_apply_device",
+    "time_kkt_apply_interleaved",
     "time_lead_terms",
     "time_rhs",
     "to_device_layout",
@@ -161,6 +166,59 @@ def _blocks(sys: TimeKKT, v: torch.Tensor):
     return g
 
 
+def _interleaved_kkt_program(sys: TimeKKT) -> DeviceProgram:
+    """The whole all-at-once operator as ONE coupling program on interleaved
+    step columns (column l*N_t + k = step k's chaos column l): the step
+    factors become diagonal N_t x N_t factors of each coupling, and the time
+    couplings M lambda_{k+1} -> r_y,k and M y_{k-1} -> r_lam,k become shifts
+    in the column space (reference operators.py:284-309)."""
+    prog = sys._cache.get("interleaved")
+    if prog is None:
+        st = sys.steady
+        n_xi, T, m, n_t, tau = st.n_xi, st.n_terms, st.mass_slice, sys.n_t, sys.tau
+        w = np.asarray(sys.stencil.weights, np.float64)
+        kr = lambda a, b: sp.kron(a, b, format="csr")
+        ix, it = sp.identity(n_xi, format="csr"), sp.identity(n_t, format="csr")
+        nxt = sp.diags(np.ones(n_t - 1), -1, shape=(n_t, n_t), format="csr")  # src step k+1 -> dst step k
+        prv = sp.diags(np.ones(n_t - 1), 1, shape=(n_t, n_t), format="csr")  # src step k-1 -> dst step k
+        full = (0, n_xi * n_t)
+        cps = [coupling_from_csr(0, 0, m, kr(st.triple.objective_weight.tocsr(), sp.diags(tau * w)), full, full, 1.0),
+               coupling_from_csr(2, 0, m, kr(ix, nxt - it), full, full, 1.0),  # M (lam_{k+1} - lam_k)
+               coupling_from_csr(1, 1, m, kr(ix, sp.diags(st.beta * tau * w)), full, full, 1.0),
+               coupling_from_csr(2, 1, m, kr(ix, it), full, full, tau),
+               coupling_from_csr(0, 2, m, kr(ix, prv - it), full, full, 1.0),  # M (y_{k-1} - y_k)
+               coupling_from_csr(1, 2, m, kr(ix, it), full, full, tau)]
+        for t in range(T):
+            h = kr(st.triple.matrices[t].tocsr(), it)
+            cps.append(coupling_from_csr(2, 0, t, h, full, full, -tau))
+            cps.append(coupling_from_csr(0, 2, t, h, full, full, -tau))
+        prog = DeviceProgram(cps, (n_xi * n_t,) * 3, n_inputs=3)
+        sys._cache["interleaved"] = prog
+    return prog
+
+
+def time_kkt_apply_interleaved(sys: TimeKKT, v: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """time_kkt_apply_device as one program launch between two transposes
+    per block ((N_t, N*n_xi) <-> (N*n_xi, N_t)); same operator, the gather
+    may sum in a different order than the per-step launches."""
+    from . import _lib
+
+    st = sys.steady
+    n_t, cells = sys.n_t, st.n_h * st.n_xi
+    lib = _lib.lib()
+    vi = torch.empty((3, st.n_h, st.n_xi * n_t), dtype=torch.float64, device=v.device)
+    oi = torch.empty_like(vi)
+    vb = v.view(3, n_t, cells)
+    ob = out.view(3, n_t, cells)
+    for b in range(3):
+        _lib.check(lib.sgk_n2f(n_t, cells, vb[b].data_ptr(), vi[b].data_ptr(), _lib.stream_ptr()), "sgk_n2f")
+    run_program(st.pattern, _interleaved_kkt_program(sys), [(vi[0], 0), (vi[1], 0), (vi[2], 0)],
+                [(oi[0], 0), (oi[1], 0), (oi[2], 0)], alpha=[1.0] * 3, beta=[0.0] * 3)
+    for b in range(3):
+        _lib.check(lib.sgk_n2f(cells, n_t, oi[b].data_ptr(), ob[b].data_ptr(), _lib.stream_ptr()), "sgk_n2f")
+    return out
+
+
 def time_kkt_apply_device(sys: TimeKKT, v: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
     g = _blocks(sys, v)
     o = _blocks(sys, out)
@@ -220,9 +278,9 @@ def time_kkt_apply(sys: TimeKKT, v):
     if isinstance(v, torch.Tensor) and v.is_cuda:
         if v.numel() != 3 * sys.block_size():
             raise ValueError("vector length does not match the system")
-        return time_kkt_apply_device(sys, v.contiguous(), torch.empty_like(v))
+        return time_kkt_apply_interleaved(sys, v.contiguous(), torch.empty_like(v))
     vd = to_device_layout(sys, v)
-    return from_device_layout(sys, time_kkt_apply_device(sys, vd, torch.empty_like(vd)))
+    return from_device_layout(sys, time_kkt_apply_interleaved(sys, vd, torch.empty_like(vd)))
 
 
 def time_rhs(sys: TimeKKT) -> np.ndarray:

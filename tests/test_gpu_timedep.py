@@ -134,3 +134,20 @@ def test_step_batched_schur_block_matches_per_step_loop(lead):
     n = len(batched) // 3
     assert np.array_equal(batched[:2 * n], stepwise[:2 * n])
     assert _rel(batched[2 * n:], stepwise[2 * n:]) <= 1e-13
+
+
+def test_interleaved_kkt_matches_per_step_launches():
+    """The all-at-once operator as one program on interleaved step columns
+    equals the per-step launches to rounding, and the reference's golden
+    output at 1e-12."""
+    import torch
+
+    from paper_2512_23804_b200.timedep import (from_device_layout, time_kkt_apply_device,
+                                               time_kkt_apply_interleaved, to_device_layout)
+
+    c, sys_, _ = _system()
+    v = to_device_layout(sys_, c["v"])
+    a = time_kkt_apply_device(sys_, v, torch.empty_like(v))
+    b = time_kkt_apply_interleaved(sys_, v, torch.empty_like(v))
+    assert float((a - b).abs().max()) <= 1e-13 * float(a.abs().max())
+    assert _rel(from_device_layout(sys_, b), c["kkt"]) <= 1e-12

@@ -45,3 +45,7 @@ for ls in ("lu", "fastdiag"):
     print(f"prec[{ls}] apply: host enqueue {w:.2f} ms, device {g:.2f} ms, {n:.0f} launches ({1e3 * w / max(n, 1):.1f} us each)")
 w, g, n = both(lambda: time_kkt_apply_device(sys_, bd, out))
 print(f"kkt apply: host enqueue {w:.2f} ms, device {g:.2f} ms, {n:.0f} launches")
+from paper_2512_23804_b200.timedep import time_kkt_apply_interleaved
+
+w, g, n = both(lambda: time_kkt_apply_interleaved(sys_, bd, out))
+print(f"kkt apply (interleaved, one program): host enqueue {w:.2f} ms, device {g:.2f} ms, {n:.0f} launches")
