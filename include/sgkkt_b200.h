@@ -304,6 +304,12 @@ int sgk_cheb_step_batched(const sgk_pattern* pat, int32_t slice, const double* s
 int sgk_colscale(int64_t n_rows, int64_t n_cols, const double* x,
                  const double* w, int32_t invert_w, double s, double* y,
                  void* stream);
+/* n_batch back-to-back (n_rows x n_cols) blocks, block b scaled by the
+ * device scalar s[b]: y = s[b] * (x / w or x * w) — the N_t steps of the
+ * PINT preconditioner's y/u blocks (preconditioners.py:278-312) at once.   */
+int sgk_colscale_batched(int64_t n_batch, int64_t n_rows, int64_t n_cols,
+                         const double* x, const double* w, int32_t invert_w,
+                         const double* s, double* y, void* stream);
 
 /* y = beta*y + mass-stencil(x)*w  etc. are expressed as programs.          */
 

@@ -148,6 +148,7 @@ _SIGNATURES = {
     "sgk_cheb_step_batched": (c_i32, [ctypes.POINTER(Pattern), c_i32, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
                                       c_vp, c_dbl, c_vp]),
     "sgk_colscale": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_i32, c_dbl, c_vp, c_vp]),
+    "sgk_colscale_batched": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "sgk_reduce_blocks": (c_i32, []),
     "sgk_dot_partial": (c_i32, [c_i64, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "sgk_reduce_partials": (c_i32, [c_vp, c_i32, c_vp, c_i32, c_vp]),

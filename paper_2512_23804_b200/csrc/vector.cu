@@ -87,6 +87,26 @@ __global__ void __launch_bounds__(256, 4) cheb_step_kernel(sgk_pattern pat, int 
   }
 }
 
+// Batched column scaling: block b of n_batch back-to-back (n_rows x n_cols)
+// blocks is scaled by the device scalar s[b] (the N_t steps of the PINT
+// preconditioner: one launch instead of one per step); per element the same
+// arithmetic as colscale_kernel.
+__global__ void colscale_batched_kernel(int64_t n_batch, int64_t n_rows, int64_t n_cols,
+                                        const double* __restrict__ x, const double* __restrict__ w, int invert,
+                                        const double* __restrict__ s, double* y) {
+  const int64_t blk = n_rows * n_cols;
+  const int64_t total = n_batch * blk;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double v = x[idx];
+    if (w) {
+      const double wk = __ldg(w + idx % n_cols);
+      v = invert ? v / wk : v * wk;
+    }
+    y[idx] = __ldg(s + idx / blk) * v;
+  }
+}
+
 __global__ void colscale_kernel(int64_t n_rows, int64_t n_cols, const double* __restrict__ x,
                                 const double* __restrict__ w, int invert, double s, double* y) {
   const int64_t total = n_rows * n_cols;
@@ -268,6 +288,17 @@ extern "C" int sgk_cheb_step(const sgk_pattern* pat, int32_t slice, const double
                              int64_t n_cols, const double* b, const double* x, const double* x_prev,
                              double* x_new, double omega, void* stream) {
   return sgk_cheb_step_batched(pat, slice, scale, 1, n_cols, b, x, x_prev, x_new, omega, stream);
+}
+
+extern "C" int sgk_colscale_batched(int64_t n_batch, int64_t n_rows, int64_t n_cols, const double* x,
+                                    const double* w, int32_t invert_w, const double* s, double* y, void* stream) {
+  SGK_REQUIRE(x && y && s, "sgk_colscale_batched: null argument");
+  SGK_REQUIRE(n_batch >= 0 && n_rows >= 0 && n_cols >= 0, "sgk_colscale_batched: negative size");
+  const int64_t total = n_batch * n_rows * n_cols;
+  if (total == 0) return SGK_OK;
+  colscale_batched_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(n_batch, n_rows, n_cols, x, w,
+                                                                                 invert_w, s, y);
+  return check_launch("colscale_batched_kernel");
 }
 
 extern "C" int sgk_colscale(int64_t n_rows, int64_t n_cols, const double* x, const double* w,

@@ -45,7 +45,7 @@ from .linalg import csr_from_coo
 from .operators import KroneckerSumOperator, SteadyKKT
 from .preconditioners import HierarchicalGaussSeidel, _richardson_device, build_sweep, make_mass_solver
 from .program import coupling_from_csr
-from .vec import colscale
+from .vec import colscale, colscale_batched
 
 __all__ = [
     "TimeKKT",
@@ -404,6 +404,18 @@ class TimeKKTPreconditioner:
             its = self.mass_solve.its
             mass_yu = dm.cheb_batched(g[0:2].reshape(2 * sys.n_t, st.n_h, st.n_xi), its).view(
                 2, sys.n_t, st.n_h, st.n_xi)
+        if batched and dm is not None:
+            # y/u column scalings of all steps: one launch each, step scalars on the device
+            sc = self._cache.get("step_scales")
+            if sc is None:
+                sc = torch.tensor([[1.0 / (tau * float(d)) for d in wsteps],
+                                   [1.0 / (st.beta * tau * float(d)) for d in wsteps]],
+                                  dtype=torch.float64, device=r.device)
+                self._cache["step_scales"] = sc
+            colscale_batched(mass_yu[0], wv, sc[0], o[0], invert=True)
+            colscale_batched(mass_yu[1], None, sc[1], o[1])
+            self._schur_all_steps(g[2], o[2])
+            return out
         for k in steps:
             dk = float(wsteps[k])
             my = mass_yu[0, k] if dm is not None else self._mass(g[0, k])

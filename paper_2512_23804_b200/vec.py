@@ -7,7 +7,7 @@ import torch
 
 from . import _lib
 
-__all__ = ["Reducer", "axpby", "colscale", "lincomb3"]
+__all__ = ["Reducer", "axpby", "colscale", "colscale_batched", "lincomb3"]
 
 
 class Reducer:
@@ -76,6 +76,21 @@ def lincomb3(out: torch.Tensor, x0: torch.Tensor, c1: float = 0.0, x1: torch.Ten
     _lib.check(lib.sgk_lincomb3(out.numel(), x0.data_ptr(), c1, x1.data_ptr() if x1 is not None else None, c2,
                                 x2.data_ptr() if x2 is not None else None, s, out.data_ptr(), _lib.stream_ptr()),
                "sgk_lincomb3")
+    return out
+
+
+def colscale_batched(x: torch.Tensor, w: torch.Tensor | None, s: torch.Tensor, out: torch.Tensor,
+                     invert: bool = False):
+    """out[b] = s[b] * (x[b] / w or x[b] * w) for a (n_b, n_rows, n_cols)
+    stack; `s` a device vector of n_b scalars.  Per element the same
+    arithmetic as `colscale`."""
+    lib = _lib.lib()
+    n_b, n_rows, n_cols = x.shape
+    if s.numel() != n_b or not (x.is_contiguous() and out.is_contiguous()):
+        raise ValueError("colscale_batched: need contiguous stacks and one scalar per block")
+    _lib.check(lib.sgk_colscale_batched(n_b, n_rows, n_cols, x.data_ptr(), w.data_ptr() if w is not None else None,
+                                        int(invert), s.data_ptr(), out.data_ptr(), _lib.stream_ptr()),
+               "sgk_colscale_batched")
     return out
 
 
