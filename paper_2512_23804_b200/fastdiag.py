@@ -159,9 +159,16 @@ class FastDiagFactors:
         st = self._dev()
         lib = _lib.lib()
         n_work = int(lib.sgk_fastdiag_work_doubles(ctypes.byref(st), int(width)))
-        work = torch.empty(max(n_work, 1), dtype=torch.float64, device=b_segs[0][0].device)
+        sp_ = _lib.stream_ptr(stream)
+        # scratch reused per stream (stream order serialises its users; grown
+        # on demand) instead of an allocation per solve
+        key = ("work", sp_)
+        work = self._cache.get(key)
+        if work is None or work.numel() < n_work or work.device != b_segs[0][0].device:
+            work = torch.empty(max(n_work, 1), dtype=torch.float64, device=b_segs[0][0].device)
+            self._cache[key] = work
         rc = lib.sgk_fastdiag_solve(ctypes.byref(st), ctypes.byref(bv), ctypes.byref(xv), work.data_ptr(),
-                                    int(width), _lib.stream_ptr(stream))
+                                    int(width), sp_)
         _lib.check(rc, "sgk_fastdiag_solve")
 
     def solve(self, b):
