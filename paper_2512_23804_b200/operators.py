@@ -174,7 +174,7 @@ def _slab_plan(op: KroneckerSumOperator, n_slabs: int):
 
 
 def _kron_apply_pipelined(op: KroneckerSumOperator, x_cpu: torch.Tensor, out_cpu: torch.Tensor,
-                          n_slabs: int = 16) -> torch.Tensor:
+                          n_slabs: int = 32) -> torch.Tensor:
     """Host buffers in and out (pinned): H2D of row slab s+1, the matvec of
     slab s and the D2H of slab s-1 run on three streams at once, so the two
     PCIe directions and the kernel overlap (the end-to-end path)."""
