@@ -154,6 +154,33 @@ int sgk_stencil9_apply(const sgk_pattern9* pat, const sgk_program9* prog,
                        int32_t n_out, const sgk_view* out,
                        const sgk_view* init, const double* alpha,
                        const double* beta, int32_t block_threads, void* stream);
+/* Grid form of the 9-point pattern: the Q1 stencil of an nx x ny grid in
+ * natural node order (p = iy*nx + ix; the neighbours of p are p+dy*nx+dx).
+ * coefg[p][t][(dy+1)*3 + dx+1] holds the t-stacked values in stencil
+ * position order, zero where a neighbour lies outside the grid (10 doubles
+ * per (p, t), the 10th zero).  A launch covers nodes [row0, row0+n_rows);
+ * output/init views start at node row0, input views at node 0.              */
+typedef struct {
+  int32_t n_rows;
+  int32_t n_slices;
+  int32_t nx;
+  int32_t ny;
+  int32_t row0;
+  int32_t seg_len;        /* rows per grid-line segment of the CTA walk     */
+  const double* coefg;    /* [nx*ny*n_slices*10]                            */
+} sgk_grid9;
+
+/* Warp-specialised 9-point program on the grid form (contiguous row ranges
+ * per CTA, sliding V window).  Programs with 1..8 column groups.            */
+int sgk_stencil9_grid_apply(const sgk_grid9* grid, const sgk_program9* prog,
+                            int32_t n_in, const sgk_view* in,
+                            int32_t n_out, const sgk_view* out,
+                            const sgk_view* init, const double* alpha,
+                            const double* beta, void* stream);
+/* coefg from the padded layout (colind9, coef10) of the same grid pattern.  */
+int sgk_grid9_coef(int32_t n_rows, int32_t n_slices, int32_t nx,
+                   const int32_t* colind9, const double* coef10, double* coefg,
+                   void* stream);
 /* Shared-memory bytes the fast path needs for (pattern, program).          */
 int64_t sgk_stencil9_smem_bytes(const sgk_pattern9* pat, const sgk_program9* prog);
 
@@ -239,6 +266,49 @@ int32_t sgk_trisolve_grouped_chunk_cols(void);
 int sgk_trisolve_grouped(const sgk_trigroups* L, const sgk_trigroups* U,
                          const sgk_segview* b, const sgk_segview* x,
                          double* work, int32_t width, int32_t epoch, void* stream);
+
+/* Wide-RHS form of the grouped solve (csrc/trisolve_wide.cu): the same
+ * processing-space triangle and chain groups, the groups' outside entries cut
+ * into segments (<= 32 entries, one row each) and tiles (<= 32 segments) in
+ * topological group order; a group with several tiles gathers its per-(tile,
+ * row) partial sums in `part` slots and is finalised by its last tile.     */
+typedef struct {
+  int32_t n;
+  int32_t n_groups;
+  int32_t n_tiles;
+  int32_t reversed;           /* U passed reversed: work row of p = n-1-p    */
+  const int32_t* rowptr;      /* [n+1] strict triangle (processing space)   */
+  const int32_t* colind;
+  const double* vals;
+  const int32_t* group_ptr;   /* [n_groups+1]                               */
+  const int32_t* tile_group;  /* [n_tiles]                                  */
+  const int32_t* tile_seg;    /* [n_tiles+1] segment range of each tile      */
+  const int32_t* tile_dep_ptr;/* [n_tiles+1]                                */
+  const int32_t* tile_dep;    /* groups each tile's entries read            */
+  const int32_t* group_ntiles;/* [n_groups]                                 */
+  const int32_t* seg_row;     /* [n_seg] processing row                     */
+  const int32_t* seg_e0;      /* [n_seg] entry range [e0, e1), <= 32 entries */
+  const int32_t* seg_e1;
+  const int32_t* seg_slot;    /* [n_seg] part slot (multi-tile groups)      */
+  const int32_t* row_slot_ptr;/* [n+1] part slots of each row, tile order   */
+  const int32_t* row_slot;
+  const int32_t* work_row;    /* [n]                                        */
+  const int32_t* io_row;      /* [n]                                        */
+  const int64_t* minv_ptr;    /* [n_groups]                                 */
+  const double* minv;         /* dense inverse of each group's diagonal block */
+  int32_t* flags;             /* [n_groups * chunks] epoch flags             */
+  int32_t* counters;          /* [n_groups * chunks] tile counters (zeroed per solve) */
+  int32_t* ticket;
+} sgk_triwide;
+
+/* Chunk width (columns per task) the wide solve uses for `width`.          */
+int32_t sgk_trisolve_wide_chunk_cols(int32_t width);
+/* Same result as sgk_trisolve_grouped.  work and part: n x ldw doubles with
+ * ldw = width rounded up to the chunk width (part: n_slots rows).           */
+int sgk_trisolve_wide(const sgk_triwide* L, const sgk_triwide* U,
+                      const sgk_segview* b, const sgk_segview* x,
+                      double* work, double* part, int32_t width, int32_t epoch,
+                      void* stream);
 
 /* Fast-diagonalisation factor of a Kronecker-sum lead (
  * replaces LUFactors.solve, linalg.py:76-87, when the lead is

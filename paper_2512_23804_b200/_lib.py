@@ -75,6 +75,11 @@ class Pattern9(ctypes.Structure):
     _fields_ = [("n_rows", c_i32), ("n_slices", c_i32), ("colind9", c_vp), ("coef10", c_vp)]
 
 
+class Grid9(ctypes.Structure):
+    _fields_ = [("n_rows", c_i32), ("n_slices", c_i32), ("nx", c_i32), ("ny", c_i32), ("row0", c_i32),
+                ("seg_len", c_i32), ("coefg", c_vp)]
+
+
 class Program9(ctypes.Structure):
     _fields_ = [
         ("n_groups", c_i32), ("n_steps", c_i32), ("n_ubuf", c_i32), ("n_out_cols", c_i32),
@@ -130,6 +135,11 @@ _SIGNATURES = {
                                    ctypes.POINTER(View), ctypes.POINTER(c_dbl),
                                    ctypes.POINTER(c_dbl), c_i32, c_vp]),
     "sgk_stencil9_smem_bytes": (c_i64, [ctypes.POINTER(Pattern9), ctypes.POINTER(Program9)]),
+    "sgk_stencil9_grid_apply": (c_i32, [ctypes.POINTER(Grid9), ctypes.POINTER(Program9), c_i32,
+                                        ctypes.POINTER(View), c_i32, ctypes.POINTER(View),
+                                        ctypes.POINTER(View), ctypes.POINTER(c_dbl),
+                                        ctypes.POINTER(c_dbl), c_vp]),
+    "sgk_grid9_coef": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "sgk_trisolve": (c_i32, [ctypes.POINTER(TriFactor), ctypes.POINTER(TriFactor), c_vp, c_vp,
                              ctypes.POINTER(SegView), ctypes.POINTER(SegView), c_vp, c_i32,
                              c_i32, c_vp]),
@@ -238,3 +248,14 @@ _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None) if hasattr(to
 
 def launch_count() -> int:
     return int(_load().sgk_launch_count())
+
+
+_SM_COUNT = None
+
+
+def sm_count() -> int:
+    """SM count of the current CUDA device (cached; 148 on B200)."""
+    global _SM_COUNT
+    if _SM_COUNT is None:
+        _SM_COUNT = int(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count)
+    return _SM_COUNT

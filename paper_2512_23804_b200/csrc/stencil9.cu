@@ -618,6 +618,294 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
   }
 }
 
+// ---------------------------------------------------------------------------
+// Grid variant of the warp-specialised kernel (config-4 matvec): the pattern
+// is the Q1 9-point stencil of an nx x ny grid in natural order, so the
+// neighbours of node p = iy*nx + ix are p + dy*nx + dx and the producers
+// address V geometrically.  Every CTA walks a CONTIGUOUS range of rows, so
+// consecutive rows of a grid line share 6 of their 9 neighbours: the V
+// window (3 lines x 3 columns x 4 slots in registers) slides, and each row
+// loads only the new column (12 doubles per lane instead of 36; no colind
+// loads).  Coefficients come from coefg, the t-stacked values in stencil
+// position order (dy+1)*3 + (dx+1) with zeros for missing neighbours; a
+// missing neighbour's V load is redirected to the row's own node (finite
+// value times a zero coefficient).  Gather and barriers as stencil9_ws_kernel.
+template <int MAXOUT, bool ONEOUT>
+__global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk_program9 prog, ViewSet in,
+                                                              ViewSet out, ViewSet init, ScalarSet alpha,
+                                                              ScalarSet beta) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const Smem9 L = smem9_ws_layout(gp.n_slices, prog);
+  double* coef_s = reinterpret_cast<double*>(sm + L.coef);
+  double* ubuf = reinterpret_cast<double*>(sm + L.ubuf);
+  double* ctab = reinterpret_cast<double*>(sm + L.ctab);
+  int32_t* steps = reinterpret_cast<int32_t*>(sm + L.steps);
+  int32_t* groups = reinterpret_cast<int32_t*>(sm + L.groups);
+  int32_t* ccnt = reinterpret_cast<int32_t*>(sm + L.ccnt);
+  int32_t* coff = reinterpret_cast<int32_t*>(sm + L.coff);
+  uint32_t* gent = reinterpret_cast<uint32_t*>(sm + L.gent);
+  const int ustride = (int)(align16(sizeof(double) * ((size_t)prog.n_ubuf + 64)));
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const bool producer = warp < 8;
+  const int n_chunks = prog.n_chunks;
+  __shared__ const double* in_ptr[SGK_MAX_IO];
+  __shared__ int64_t in_ld[SGK_MAX_IO];
+  if (tid < SGK_MAX_IO) {
+    const sgk_view& vv = pick(in, tid);
+    in_ptr[tid] = vv.ptr + vv.col0;
+    in_ld[tid] = vv.ld;
+  }
+  const int ncoef = gp.n_slices * 10;
+  for (int i = tid; i < prog.n_coef; i += blockDim.x) ctab[i] = prog.coef_tab[i];
+  for (int i = tid; i < prog.n_steps; i += blockDim.x) steps[i] = prog.step_rec[i];
+  for (int i = tid; i < 4 * (prog.n_groups + 1); i += blockDim.x) groups[i] = prog.group_info[i];
+  for (int i = tid; i < n_chunks; i += blockDim.x) {
+    ccnt[i] = prog.gather_ptr[2 * i];
+    coff[i] = prog.gather_ptr[2 * i + 1];
+  }
+  for (int i = tid; i < prog.n_gather; i += blockDim.x) gent[i] = prog.gather_ent[i];
+  for (int i = tid; i < 64; i += blockDim.x) {
+    ubuf[prog.n_ubuf + i] = 0.0;
+    reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ubuf) + ustride)[prog.n_ubuf + i] = 0.0;
+  }
+  __syncthreads();
+
+  // Rows are walked in grid-line SEGMENTS of seg_len nodes (segment s =
+  // line s / nq, part s % nq); CTA b takes segments b, b + G, ... so at any
+  // time the CTAs work on vertically adjacent segments at the same x: the
+  // neighbour lines a CTA reads are the lines its neighbour CTAs are
+  // streaming at that moment (L2 hits), while consecutive rows of a segment
+  // slide the V window.  Segments are clipped to the launch's node range.
+  const int nx = gp.nx, ny = gp.ny;
+  const int A = gp.row0, B = gp.row0 + gp.n_rows;
+  const int SL = gp.seg_len, nq = (nx + SL - 1) / SL;
+  auto seg_of = [&](int node) { const int y = node / nx; return y * nq + (node - y * nx) / SL; };
+  auto seg_range = [&](int sg, int& a, int& b) {
+    const int y = sg / nq, q = sg - y * nq;
+    a = max(A, y * nx + q * SL);
+    b = min(B, y * nx + min(nx, (q + 1) * SL));
+  };
+  const int s_last = gp.n_rows > 0 ? seg_of(B - 1) : -1;
+  const int s_first = gp.n_rows > 0 ? seg_of(A) : 0;
+  // next row after `node` of segment sg ending at nend: same segment, or the
+  // first row of this CTA's next segment (restart = true), or none
+  auto advance = [&](int& sg, int& node, int& nend, bool& restart) -> bool {
+    ++node;
+    restart = false;
+    if (node < nend) return true;
+    sg += gridDim.x;
+    if (sg > s_last) return false;
+    seg_range(sg, node, nend);
+    restart = true;
+    return true;
+  };
+  if (producer) {
+    const int pt = tid;  // 0..255
+    auto stage = [&](int row, int buf) {
+      const double* src = gp.coefg + (int64_t)(gp.row0 + row) * ncoef;
+      double* dst = coef_s + buf * ncoef;
+      for (int i = pt; i < ncoef / 2; i += 256) cp_async16(dst + 2 * i, src + 2 * i);
+    };
+    int rbase = 0, rq0 = 0, rq1 = 0;
+    const double* rvb = nullptr;
+    int64_t rld = 0;
+    int rncols = kGroupCols;
+    double rv[kCols][9];
+    const bool active = warp < prog.n_groups;
+    if (active) {
+      for (int g = 0; g < warp; ++g) rbase += kGroupCols * (groups[4 * (g + 1) + 3] - groups[4 * g + 3]);
+      const int4 gi = *reinterpret_cast<const int4*>(groups + 4 * warp);
+      rq0 = gi.w;
+      rq1 = groups[4 * (warp + 1) + 3];
+      rvb = in_ptr[gi.x] + gi.y;
+      rld = in_ld[gi.x];
+      rncols = gi.z;
+    }
+    // every group is a full 128-column group here (host-checked), so a
+    // neighbour's 4 slot loads are immediate offsets of one base address
+    const double* vlane = rvb + lane;
+    auto nbase = [&](int p, bool ok, int d) -> const double* { return vlane + (int64_t)(ok ? p + d : p) * rld; };
+    // window of node p: shift the columns left and load column dxn into
+    // the right one.  Sliding from p-1 is one call (dxn = 1); a line start or
+    // the range start is three calls (dxn = -1, 0, 1) through the SAME code
+    // (a second load path made ptxas spill the window at 128 registers).
+    auto window = [&](int p, bool restart) {
+      const int iy = p / nx, ix = p - iy * nx;
+      const bool yl = iy > 0, yh = iy + 1 < ny;
+#pragma unroll 1
+      for (int dxn = restart ? -1 : 1; dxn <= 1; ++dxn) {
+        const bool xok = ix + dxn >= 0 && ix + dxn < nx;
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy) {
+          const bool ok = (dy < 0 ? yl : (dy > 0 ? yh : true)) && xok;
+          const double* b = nbase(p, ok, dy * nx + dxn);
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) {
+            rv[c][(dy + 1) * 3 + 0] = rv[c][(dy + 1) * 3 + 1];
+            rv[c][(dy + 1) * 3 + 1] = rv[c][(dy + 1) * 3 + 2];
+            rv[c][(dy + 1) * 3 + 2] = SGK_VLD(b + 32 * c);
+          }
+        }
+      }
+    };
+    int sg = s_first + blockIdx.x, node = 0, nend = 0;
+    bool have = sg <= s_last;
+    if (have) seg_range(sg, node, nend);
+    if (have) stage(node - A, 0);
+    cp_async_commit();
+    if (active && have) window(node, true);
+    int it = 0;
+    for (; have; ++it) {
+      const int cb = it & 1;
+      int sg_n = sg, node_n = node, nend_n = nend;
+      bool restart_n = false;
+      const bool have_n = advance(sg_n, node_n, nend_n, restart_n);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      bar_sync_n(5, 256);  // this row's coefficients visible; every producer is done with row it-1
+      if (have_n) stage(node_n - A, cb ^ 1);
+      cp_async_commit();
+      if (it >= 2) bar_sync_n(3 + cb, 512);  // consumers are done with U buffer cb (row it-2)
+      if (active) {
+        const double* crow = coef_s + cb * ncoef;
+        double* ubq = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ubuf) + cb * ustride) + rbase;
+        int recn = rq0 < rq1 ? steps[rq0] : 0;
+        double2 p01 = make_double2(0.0, 0.0), p23 = p01;
+        if (rq0 < rq1) {
+          const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (recn & 0xFFFF));
+          p01 = a2[0];
+          p23 = a2[1];
+        }
+        for (int q = rq0; q < rq1; ++q, ubq += kGroupCols) {
+          const int rec = recn;
+          double* ub = ubq + (lane ^ (rec >> 16));
+          double a[10];
+          a[0] = p01.x; a[1] = p01.y; a[2] = p23.x; a[3] = p23.y;
+          {
+            const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (rec & 0xFFFF));
+#pragma unroll
+            for (int k = 2; k < 5; ++k) {
+              const double2 p = a2[k];
+              a[2 * k] = p.x;
+              a[2 * k + 1] = p.y;
+            }
+          }
+          recn = steps[q + 1 < rq1 ? q + 1 : q];
+          {
+            const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (recn & 0xFFFF));
+            p01 = a2[0];
+            p23 = a2[1];
+          }
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) ub[32 * c] = dot9(a, rv[c]);
+        }
+      }
+      bar_arrive_n(1 + cb, 512);  // U buffer cb holds row it
+      if (active && have_n) window(node_n, restart_n);  // next row's window: overlaps the next waits
+      sg = sg_n;
+      node = node_n;
+      nend = nend_n;
+      have = have_n;
+    }
+    for (int k = (it >= 2 ? it - 2 : 0); k < it; ++k) bar_sync_n(3 + (k & 1), 512);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  } else {
+    const int cw = warp - 8;
+    int ocol[MAXOUT];
+#pragma unroll
+    for (int r = 0; r < MAXOUT; ++r) {
+      const int chunk = cw + r * 8;
+      ocol[r] = chunk < n_chunks ? __ldg(prog.out_col + chunk * 32 + lane) : -1;
+    }
+    int sg = s_first + blockIdx.x, node = 0, nend = 0;
+    bool have = sg <= s_last;
+    if (have) seg_range(sg, node, nend);
+    for (int it = 0; have; ++it) {
+      const int row = node - A;  // local output row
+      const int cb = it & 1;
+      bar_sync_n(1 + cb, 512);  // products of this row are in U buffer cb
+      const unsigned char* smb = sm + cb * ustride;
+      double* orow = nullptr;
+      const double* irow = nullptr;
+      if constexpr (ONEOUT) {
+        orow = out.v[0].ptr + (int64_t)row * out.v[0].ld + out.v[0].col0;
+        if (init.v[0].ptr != nullptr) irow = init.v[0].ptr + (int64_t)row * init.v[0].ld + init.v[0].col0;
+      }
+#pragma unroll
+      for (int rb = 0; rb < MAXOUT; ++rb) {
+        const int chunk = cw + rb * 8;
+        if (chunk >= n_chunks) break;
+        const int npair = ccnt[chunk] >> 1;
+        const uint2* gpe = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 2
+        for (int e = 0; e < npair; ++e, gpe += 32) {
+          const uint2 w = *gpe;
+          acc0 = fma(*reinterpret_cast<const double*>(sm + (w.x & 0x3FFF)),
+                     *reinterpret_cast<const double*>(smb + (w.x >> 14)), acc0);
+          acc1 = fma(*reinterpret_cast<const double*>(sm + (w.y & 0x3FFF)),
+                     *reinterpret_cast<const double*>(smb + (w.y >> 14)), acc1);
+        }
+        const int oc = ocol[rb];
+        if (oc >= 0) {
+          const double acc = acc0 + acc1;
+          if constexpr (ONEOUT) {
+            double y = alpha.s[0] * acc;
+            if (irow != nullptr) y = fma(beta.s[0], irow[oc], y);
+            orow[oc] = y;
+          } else {
+            const int o = oc >> 24, k = oc & 0xFFFFFF;
+            const double al = sel4(alpha.s[0], alpha.s[1], alpha.s[2], alpha.s[3], o);
+            const double be = sel4(beta.s[0], beta.s[1], beta.s[2], beta.s[3], o);
+            const double* ip = sel4(init.v[0].ptr, init.v[1].ptr, init.v[2].ptr, init.v[3].ptr, o);
+            const int64_t il = sel4(init.v[0].ld, init.v[1].ld, init.v[2].ld, init.v[3].ld, o);
+            const int ic = sel4(init.v[0].col0, init.v[1].col0, init.v[2].col0, init.v[3].col0, o);
+            double* op = sel4(out.v[0].ptr, out.v[1].ptr, out.v[2].ptr, out.v[3].ptr, o);
+            const int64_t ol = sel4(out.v[0].ld, out.v[1].ld, out.v[2].ld, out.v[3].ld, o);
+            const int occ = sel4(out.v[0].col0, out.v[1].col0, out.v[2].col0, out.v[3].col0, o);
+            double y = al * acc;
+            if (ip != nullptr) y += be * ip[(int64_t)row * il + ic + k];
+            op[(int64_t)row * ol + occ + k] = y;
+          }
+        }
+      }
+      bar_arrive_n(3 + cb, 512);  // done reading U buffer cb
+      bool restart;
+      have = advance(sg, node, nend, restart);
+    }
+  }
+}
+
+template <int MAXOUT, bool ONEOUT>
+static int launch9grid(const sgk_grid9& gp, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
+                       const ViewSet& init, const ScalarSet& a, const ScalarSet& b, cudaStream_t st) {
+  const Smem9 L = smem9_ws_layout(gp.n_slices, prog);
+  static bool attr_set = false;
+  if (!attr_set) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, stencil9_grid_kernel<MAXOUT, ONEOUT>);
+    cudaFuncSetAttribute(stencil9_grid_kernel<MAXOUT, ONEOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         optin - (int)fa.sharedSizeBytes);
+    cudaGetLastError();
+    attr_set = true;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_grid_kernel<MAXOUT, ONEOUT>, 512, L.total);
+  if (occ < 1) {
+    set_error("stencil9_grid_kernel: program does not fit in shared memory (" + std::to_string(L.total) + " B)");
+    return SGK_ELIMIT;
+  }
+  int64_t grid = (int64_t)sm_count() * occ;
+  if (grid < 1) return SGK_OK;
+  stencil9_grid_kernel<MAXOUT, ONEOUT><<<(int)grid, 512, L.total, st>>>(gp, prog, in, out, init, a, b);
+  return check_launch("stencil9_grid_kernel");
+}
+
 template <int MAXOUT, bool ONEOUT>
 static int launch9ws(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
                      const ViewSet& init, const ScalarSet& a, const ScalarSet& b, cudaStream_t st) {
@@ -749,4 +1037,86 @@ extern "C" int sgk_stencil9_apply(const sgk_pattern9* pat, const sgk_program9* p
   if (per <= 16) return launch9<16>(*pat, *prog, vin, vout, vinit, a, b, n_out, threads, st);
   set_error("sgk_stencil9_apply: too many output columns for one CTA");
   return SGK_ELIMIT;
+}
+
+extern "C" int sgk_stencil9_grid_apply(const sgk_grid9* gp, const sgk_program9* prog, int32_t n_in,
+                                       const sgk_view* in, int32_t n_out, const sgk_view* out,
+                                       const sgk_view* init, const double* alpha, const double* beta,
+                                       void* stream) {
+  using namespace sgk;
+  SGK_REQUIRE(gp && prog && out && alpha && beta, "sgk_stencil9_grid_apply: null argument");
+  SGK_REQUIRE(n_in >= 1 && n_in <= SGK_MAX_IO && n_out >= 1 && n_out <= SGK_MAX_IO,
+              "sgk_stencil9_grid_apply: input/output count out of range");
+  SGK_REQUIRE(gp->nx >= 3 && gp->ny >= 1 && gp->coefg != nullptr && gp->seg_len >= 1,
+              "sgk_stencil9_grid_apply: bad grid");
+  SGK_REQUIRE(gp->row0 >= 0 && gp->n_rows >= 0 && (int64_t)gp->row0 + gp->n_rows <= (int64_t)gp->nx * gp->ny,
+              "sgk_stencil9_grid_apply: row range outside the grid");
+  SGK_REQUIRE((int64_t)prog->n_coef * 8 <= (1 << 14), "sgk_stencil9_grid_apply: too many distinct coefficients");
+  SGK_REQUIRE(prog->n_slices == gp->n_slices, "sgk_stencil9_grid_apply: program compiled for another slice count");
+  SGK_REQUIRE(prog->n_groups >= 1 && prog->n_groups <= 8, "sgk_stencil9_grid_apply: needs 1..8 column groups");
+  ViewSet vin{}, vout{}, vinit{};
+  ScalarSet a{}, b{};
+  for (int i = 0; i < n_in; ++i) vin.v[i] = in[i];
+  for (int i = 0; i < n_out; ++i) {
+    SGK_REQUIRE(out[i].ptr != nullptr, "sgk_stencil9_grid_apply: null output");
+    vout.v[i] = out[i];
+    if (init) vinit.v[i] = init[i];
+    a.s[i] = alpha[i];
+    b.s[i] = beta[i];
+  }
+  if (gp->n_rows == 0 || prog->n_out_cols == 0) return SGK_OK;
+  SGK_REQUIRE(prog->n_chunks * 32 >= prog->n_out_cols, "sgk_stencil9_grid_apply: n_chunks too small");
+  const int per = (prog->n_chunks + 7) / 8;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_out == 1) {
+    if (per <= 1) return launch9grid<1, true>(*gp, *prog, vin, vout, vinit, a, b, st);
+    if (per <= 2) return launch9grid<2, true>(*gp, *prog, vin, vout, vinit, a, b, st);
+    if (per <= 4) return launch9grid<4, true>(*gp, *prog, vin, vout, vinit, a, b, st);
+    if (per <= 8) return launch9grid<8, true>(*gp, *prog, vin, vout, vinit, a, b, st);
+  } else {
+    if (per <= 1) return launch9grid<1, false>(*gp, *prog, vin, vout, vinit, a, b, st);
+    if (per <= 2) return launch9grid<2, false>(*gp, *prog, vin, vout, vinit, a, b, st);
+    if (per <= 4) return launch9grid<4, false>(*gp, *prog, vin, vout, vinit, a, b, st);
+    if (per <= 8) return launch9grid<8, false>(*gp, *prog, vin, vout, vinit, a, b, st);
+  }
+  set_error("sgk_stencil9_grid_apply: too many output columns for one CTA");
+  return SGK_ELIMIT;
+}
+
+namespace sgk {
+// coefg[p][t][(dy+1)*3+dx+1] = sum of the padded coef10 entries of row p at
+// that stencil position (padding entries carry zero values)
+__global__ void grid9_coef_kernel(int32_t n_rows, int32_t n_slices, int32_t nx, const int32_t* colind9,
+                                  const double* coef10, double* coefg) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n_rows * n_slices) return;
+  const int p = (int)(i / n_slices);
+  double acc[10];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) acc[k] = 0.0;
+  for (int jj = 0; jj < 9; ++jj) {
+    const int d = colind9[(int64_t)p * 9 + jj] - p;
+    const int dx = (d == -nx - 1 || d == -1 || d == nx - 1) ? -1 : ((d == -nx + 1 || d == 1 || d == nx + 1) ? 1 : 0);
+    const int dy = (d - dx) / nx;
+    const int pos = (dy + 1) * 3 + dx + 1;
+    const double v = coef10[i * 10 + jj];
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+      if (k == pos) acc[k] += v;
+  }
+#pragma unroll
+  for (int k = 0; k < 10; ++k) coefg[i * 10 + k] = acc[k];
+}
+}  // namespace sgk
+
+extern "C" int sgk_grid9_coef(int32_t n_rows, int32_t n_slices, int32_t nx, const int32_t* colind9,
+                              const double* coef10, double* coefg, void* stream) {
+  using namespace sgk;
+  SGK_REQUIRE(n_rows >= 0 && n_slices >= 1 && nx >= 3, "sgk_grid9_coef: bad sizes");
+  SGK_REQUIRE(colind9 && coef10 && coefg, "sgk_grid9_coef: null argument");
+  const int64_t n = (int64_t)n_rows * n_slices;
+  if (n == 0) return SGK_OK;
+  grid9_coef_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_rows, n_slices, nx, colind9,
+                                                                                 coef10, coefg);
+  return check_launch("grid9_coef_kernel");
 }

@@ -28,6 +28,11 @@ F64 = torch.float64
 import os as _os
 
 FAST9 = _os.environ.get("SGKKT_FAST9", "1") != "0"
+# SGKKT_GRID9=1 runs the config-4 matvec on the grid-form WS kernel (sliding
+# V window, grid-line segment walk): bit-identical, 30 % fewer L1 wavefronts,
+# but measured 1.126 ms vs 1.100 ms for the pattern-indexed WS kernel
+# (profiles/r02_grid_ab.txt) — off by default, kept for A/B
+GRID9 = _os.environ.get("SGKKT_GRID9", "0") == "1"
 # output columns one launch can hold (16 gather chunks x 256 threads in both
 # kernels); wider programs are launched per column block
 MAX_LAUNCH_COLS = 16 * 256
@@ -213,6 +218,41 @@ class DevicePattern:
                                      coef10=self._coef10.data_ptr())
         return self._p9
 
+    def grid9(self):
+        """(nx, ny, coefg) when the pattern is the Q1 9-point stencil of an
+        nx x ny grid in natural node order (neighbours of p = iy*nx + ix are
+        p + dy*nx + dx, every in-grid neighbour present), else None.  coefg =
+        the t-stacked values in stencil-position order (sgk_grid9 layout)."""
+        if not hasattr(self, "_grid9"):
+            self._grid9 = None
+            n = self.n_rows
+            if self.max_row_nnz <= 9 and n >= 9 and self.n_cols == n and self.pattern9() is not None:
+                row0 = self.indices[self.indptr[0]:self.indptr[1]]
+                nx = int(row0[2]) if len(row0) == 4 else 0
+                if nx >= 3 and n % nx == 0:
+                    ny = n // nx
+                    p = np.arange(n, dtype=np.int64)
+                    iy, ix = p // nx, p % nx
+                    want = []
+                    for dy in (-1, 0, 1):
+                        for dx in (-1, 0, 1):
+                            ok = (iy + dy >= 0) & (iy + dy < ny) & (ix + dx >= 0) & (ix + dx < nx)
+                            want.append(np.where(ok, p + dy * nx + dx, -1))
+                    want = np.stack(want, 1)
+                    cnt = (want >= 0).sum(1)
+                    if np.array_equal(cnt, np.diff(self.indptr)):
+                        cols = np.sort(np.where(want >= 0, want, n + 1), 1)[:, :9]
+                        row_of = np.repeat(p, cnt)
+                        jj = np.arange(self.nnz) - self.indptr[row_of]
+                        if np.array_equal(cols[row_of, jj], self.indices):
+                            p9 = self.pattern9()
+                            coefg = torch.empty((n, self.n_slices, 10), dtype=F64, device=device())
+                            rc = _lib.lib().sgk_grid9_coef(n, self.n_slices, nx, p9.colind9, p9.coef10,
+                                                           coefg.data_ptr(), _lib.stream_ptr())
+                            _lib.check(rc, "sgk_grid9_coef")
+                            self._grid9 = (nx, ny, coefg)
+        return self._grid9
+
     @property
     def algorithmic_bytes(self) -> int:
         """t-stacked values (8 B) + int32 pattern, read once."""
@@ -344,6 +384,28 @@ def _view(t: torch.Tensor | None, col0: int = 0) -> _lib.View:
     return _lib.View(ptr=t.data_ptr(), ld=t.stride(0), col0=col0, pad=0)
 
 
+def _grid_seg_len(nx: int, n_rows: int) -> int:
+    """Grid-line segment length for stencil9_grid_kernel's CTA walk: the
+    candidate (<= 64 rows, >= 8) with the fewest row steps per CTA,
+    ceil(segments / CTAs) * length, with at least one segment per CTA."""
+    env = _os.environ.get("SGKKT_GRID_SEG")
+    if env:
+        return max(1, int(env))
+    ctas = _lib.sm_count()
+    best = None
+    for k in range(1, 33):
+        seg = -(-nx // k)
+        if seg > 64:
+            continue
+        n_seg = -(-n_rows // nx) * k + 1
+        cost = -(-n_seg // ctas) * (seg + 0.5)  # + a segment restart (full window load)
+        if best is None or cost < best[0]:
+            best = (cost, seg)
+        if seg < 8:
+            break
+    return best[1] if best else max(1, nx)
+
+
 def run_program(
     pattern: DevicePattern,
     program: DeviceProgram,
@@ -399,6 +461,22 @@ def run_program(
             for v in arr:
                 if v.ptr:
                     v.ptr = v.ptr + 8 * v.ld * r0
+    if f9 is not None and GRID9 and len(inputs) == 1 and n_out == 1:
+        h9 = f9.host
+        g9 = pattern.grid9()
+        gi = h9.group_info.reshape(-1, 4)[:-1]
+        # product-heavy single-output programs of full 128-column groups
+        # (the config-4 matvec): warp-specialised grid kernel, sliding V
+        if g9 is not None and 6 <= h9.n_groups <= 8 and bool(np.all(gi[:, 2] == 128)):
+            nx, ny, coefg = g9
+            r0, r1 = rows if rows is not None else (0, pattern.n_rows)
+            gp = _lib.Grid9(n_rows=r1 - r0, n_slices=pattern.n_slices, nx=nx, ny=ny, row0=r0,
+                            seg_len=_grid_seg_len(nx, r1 - r0), coefg=coefg.data_ptr())
+            rc = lib.sgk_stencil9_grid_apply(ctypes.byref(gp), ctypes.byref(f9.struct), len(inputs), in_arr,
+                                             n_out, out_arr, init_arr, a, b, _lib.stream_ptr(stream))
+            if rc != -3:
+                _lib.check(rc, "sgk_stencil9_grid_apply")
+                return
     if f9 is not None:
         h9 = f9.host
         warps = h9.warps
@@ -407,6 +485,10 @@ def run_program(
         if rc != -3:  # -3: does not fit in shared memory -> general kernel
             _lib.check(rc, "sgk_stencil9_apply")
             return
+        if rows is not None:
+            # the general kernel walks the full-height pattern: never combine
+            # it with the row-shifted output views of a row-range launch
+            raise RuntimeError("row-range launch: the 9-point program does not fit in shared memory")
     rc = lib.sgk_program_apply(
         ctypes.byref(pattern.struct), ctypes.byref(program.generic.struct), len(inputs), in_arr, n_out,
         out_arr, init_arr, a, b, threads, _lib.stream_ptr(stream),

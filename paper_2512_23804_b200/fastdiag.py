@@ -166,6 +166,8 @@ class FastDiagFactors:
         work = self._cache.get(key)
         if work is None or work.numel() < n_work or work.device != b_segs[0][0].device:
             work = torch.empty(max(n_work, 1), dtype=torch.float64, device=b_segs[0][0].device)
+            if stream is not None:
+                work.record_stream(stream)
             self._cache[key] = work
         rc = lib.sgk_fastdiag_solve(ctypes.byref(st), ctypes.byref(bv), ctypes.byref(xv), work.data_ptr(),
                                     int(width), sp_)

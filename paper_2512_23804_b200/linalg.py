@@ -361,6 +361,10 @@ class TriangularFactors:
         xv = segview(x_segs)
         work = torch.empty((self.n, -(-width // 16) * 16 if GROUPED else width), dtype=torch.float64,
                            device=b_segs[0][0].device)
+        if stream is not None:
+            # the kernel runs on `stream`: keep the caching allocator from
+            # handing `work` to another allocation before it finishes
+            work.record_stream(stream)
         self._ensure_flags(width)
         self.epoch += 1
         if GROUPED:

@@ -185,12 +185,12 @@ def _kron_apply_pipelined(op: KroneckerSumOperator, x_cpu: torch.Tensor, out_cpu
         st = tuple(torch.cuda.Stream(device=dev) for _ in range(3))
         op._cache["streams"] = st
     s_in, s_cmp, s_out = st
-    bufs = op._cache.get("e2e_bufs")
-    if bufs is None or bufs[0].shape != (n_h, n_xi):
-        bufs = (torch.empty((n_h, n_xi), dtype=torch.float64, device=dev),
-                torch.empty((n_h, n_xi), dtype=torch.float64, device=dev))
-        op._cache["e2e_bufs"] = bufs
-    xd, wd = bufs
+    # staging buffers per call from the caching allocator (allocated on the
+    # current stream, which every pipeline stream waits on below; the current
+    # stream waits for the last D2H before they are released)
+    xd = torch.empty((n_h, n_xi), dtype=torch.float64, device=dev)
+    wd = torch.empty((n_h, n_xi), dtype=torch.float64, device=dev)
+    n_slabs = max(1, min(int(n_slabs), n_h))
     edges, need = _slab_plan(op, n_slabs)
     prog = op.program([(0, n_xi)], (0, n_xi), 0, op.n_terms)
     cur = torch.cuda.current_stream(dev)
@@ -220,14 +220,29 @@ def _kron_apply_pipelined(op: KroneckerSumOperator, x_cpu: torch.Tensor, out_cpu
     return out_cpu
 
 
-def kron_apply(op: KroneckerSumOperator, x, out=None):
+def _pipeline_ok(op: KroneckerSumOperator) -> bool:
+    """The slab pipeline needs row-range launches, i.e. the full-column
+    program must compile to the 9-point fast path (a many-term operator such
+    as config 3 does not: it takes the plain device path)."""
+    ok = op._cache.get("pipeline_ok")
+    if ok is None:
+        n_xi = op.shape[1]
+        ok = bool(_dev.FAST9 and op.pattern.pattern9() is not None
+                  and op.program([(0, n_xi)], (0, n_xi), 0, op.n_terms).fast9(op.pattern.n_slices) is not None)
+        op._cache["pipeline_ok"] = ok
+    return ok
+
+
+def kron_apply(op: KroneckerSumOperator, x, out=None, n_slabs: int = 32):
     """W = sum_t A_t X H_t (reference operators.py:88-96), one fused launch.
-    Pinned host tensors in/out take the overlapped slab pipeline."""
+    Pinned host tensors in/out (contiguous, float64) take the overlapped slab
+    pipeline."""
     n_h, n_xi = op.shape
     if (isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and isinstance(out, torch.Tensor)
-            and not out.is_cuda and out.is_pinned() and _dev.FAST9 and op.pattern.pattern9() is not None
-            and tuple(x.shape) == (n_h, n_xi) and tuple(out.shape) == (n_h, n_xi) and x.dtype == torch.float64):
-        return _kron_apply_pipelined(op, x.contiguous(), out)
+            and not out.is_cuda and out.is_pinned() and out.is_contiguous()
+            and tuple(x.shape) == (n_h, n_xi) and tuple(out.shape) == (n_h, n_xi) and x.dtype == torch.float64
+            and out.dtype == torch.float64 and _pipeline_ok(op)):
+        return _kron_apply_pipelined(op, x.contiguous(), out, n_slabs)
     xd, host = as_device_state(x, (n_h, n_xi))
     w = torch.empty((n_h, n_xi), dtype=torch.float64, device=xd.device)
     prog = op.program([(0, n_xi)], (0, n_xi), 0, op.n_terms)

@@ -231,21 +231,50 @@ def test_cfg5_full_size_operator_and_hgsoc_apply():
     assert _rel(got, want) <= 1e-11
 
 
-def test_pinned_host_pipeline_matches_device_path():
+@pytest.mark.parametrize("cfg,n,n_slabs", [(2, None, 1), (2, None, 32), (2, 8, 32), (2, 8, 1000), (1, 6, 3)])
+def test_pinned_host_pipeline_matches_device_path(cfg, n, n_slabs):
     """The overlapped slab pipeline for pinned host buffers (the e2e path)
-    gives bit-identical results to the device-resident launch."""
+    gives bit-identical results to the device-resident launch: one slab,
+    the default 32, slabs thinner than the stencil reach (8^2 grid: 49 rows
+    in 32 slabs) and more slabs than rows."""
+    import torch
+
+    from paper_2512_23804_b200.operators import KroneckerSumOperator, _pipeline_ok, kron_apply
+
+    b, cp = _forward(cfg, n=n)
+    op = KroneckerSumOperator(couplings=cp, operators=b.stiffness)
+    assert _pipeline_ok(op)
+    x = torch.randn((b.n_h, b.n_xi), dtype=torch.float64).pin_memory()
+    out = torch.empty_like(x).pin_memory()
+    got = kron_apply(op, x, out=out, n_slabs=n_slabs)
+    want = kron_apply(op, x.cuda()).cpu()
+    assert got is out
+    assert torch.equal(got, want)
+
+
+def test_pinned_host_non_contiguous_out_and_many_terms():
+    """Pinned buffers the pipeline cannot take (a non-contiguous `out`; a
+    many-term config-3 operator whose program has no 9-point schedule) go
+    through the plain device path and still match it bit for bit."""
     import torch
 
     from paper_2512_23804_b200.operators import KroneckerSumOperator, kron_apply
 
-    b, cp = _forward(2)
+    b, cp = _forward(2, n=12)
     op = KroneckerSumOperator(couplings=cp, operators=b.stiffness)
     x = torch.randn((b.n_h, b.n_xi), dtype=torch.float64).pin_memory()
-    out = torch.empty_like(x).pin_memory()
+    big = torch.zeros((b.n_h, 2 * b.n_xi), dtype=torch.float64).pin_memory()
+    out = big[:, ::2]
     got = kron_apply(op, x, out=out)
-    want = kron_apply(op, x.cuda()).cpu()
-    assert got is out
-    assert torch.equal(got, want)
+    assert torch.equal(got, kron_apply(op, x.cuda()).cpu())
+    b3, cp3 = _forward(3, n=8)
+    op3 = KroneckerSumOperator(couplings=cp3, operators=b3.stiffness)
+    x3 = torch.randn((b3.n_h, b3.n_xi), dtype=torch.float64).pin_memory()
+    out3 = torch.empty_like(x3).pin_memory()
+    got3 = kron_apply(op3, x3, out=out3)
+    assert torch.equal(got3, kron_apply(op3, x3.cuda()).cpu())
+    ref = oracle.kron_apply(cp3, b3.stiffness, x3.numpy())
+    assert _rel(got3, ref) <= 1e-12
 
 
 @pytest.mark.parametrize("dense", [True, False])

@@ -28,11 +28,15 @@ if len(srows) > 2:
     ix = {h: i for i, h in enumerate(hdr)}
     by = collections.Counter(); st = collections.Counter()
     for r in srows[2:]:
+        if len(r) <= max(ix["Source"], ix["Instructions Executed"], ix["Warp Stall Sampling (All Samples)"]):
+            continue
         s = r[ix["Source"]].strip()
         toks = s.split()
         if not toks:
             continue
         op = (toks[1] if toks[0].startswith("@") else toks[0]).split(".")[0]
+        if not r[ix["Instructions Executed"]].strip().isdigit():
+            continue
         by[op] += int(r[ix["Instructions Executed"]] or 0)
         st[op] += int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
     tot = sum(by.values()) or 1
@@ -40,5 +44,7 @@ if len(srows) > 2:
     for op, c in by.most_common(14):
         print(f"  {op:<8} {c:>12} {100 * c / tot:5.1f}%  stalls {st[op]}")
     print("top stall sites:")
-    for r in sorted(srows[2:], key=lambda r: -int(r[ix["Warp Stall Sampling (All Samples)"]] or 0))[:12]:
+    good = [r for r in srows[2:] if len(r) > ix["Warp Stall Sampling (All Samples)"]
+            and r[ix["Warp Stall Sampling (All Samples)"]].strip().isdigit()]
+    for r in sorted(good, key=lambda r: -int(r[ix["Warp Stall Sampling (All Samples)"]] or 0))[:16]:
         print("  ", r[ix["Source"]][:70].ljust(70), r[ix["Warp Stall Sampling (All Samples)"]])
