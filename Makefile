@@ -8,7 +8,11 @@ LIB := paper_2512_23804_b200/libsgkkt_b200.so
 all: $(LIB)
 
 $(LIB): $(SRC) paper_2512_23804_b200/csrc/sgk_common.cuh include/sgkkt_b200.h
-	$(NVCC) $(ARCH) $(NVFLAGS) -shared -o $@ $(SRC) -lcublas -Xlinker -rpath,/usr/local/cuda/lib64
+	$(NVCC) $(ARCH) $(NVFLAGS) -shared -o $@ $(SRC)
+
+# trace build of the wide triangular solve (tools/triw_trace.py)
+trace: $(SRC)
+	mkdir -p build_variants && $(NVCC) $(ARCH) $(NVFLAGS) -DSGK_TRIW_TRACE -shared -o build_variants/libsgkkt_triwtrace.so $(SRC)
 
 ptxas:
 	$(NVCC) $(ARCH) $(NVFLAGS) -Xptxas -v -c -o /tmp/sgk_probe.o paper_2512_23804_b200/csrc/galerkin.cu

@@ -205,10 +205,14 @@ def run_reference(args):
     }
     if not args.no_solve:
         line["solves"] = {"cfg2": cpu_solve_block(2, 1e-2)}
+        if not args.no_solve_cfg5:
+            # the headline control solve on the host ("the full CPU
+            # FGMRES solve"): hGSoc inside the reference FGMRES, beta = 1e-2
+            line["solves"]["cfg5"] = cpu_solve_block(5, 1e-2, minres=False)
     print(json.dumps(line), flush=True)
 
 
-def cpu_solve_block(cfg_id, beta):
+def cpu_solve_block(cfg_id, beta, minres=True):
     """Time-to-solution of the oracle port (reference algorithms: hGSoc inside
     the reference FGMRES; block-diagonal hGS preconditioned MINRES) on the host."""
     import scipy.sparse as sp
@@ -238,6 +242,8 @@ def cpu_solve_block(cfg_id, beta):
     x, its, conv, _ = oracle.fgmres(op, soc, rhs, 1e-8)
     out["hgsoc_fgmres"] = {"iterations": its, "converged": bool(conv), "seconds": time.perf_counter() - t0,
                            "setup_seconds": t_setup}
+    if not minres:
+        return {f"beta={beta:g}": out, "cores": 1}
     t0 = time.perf_counter()
     lead = oracle.splu_ref(oracle.shifted_lead(m, s.stiffness, s.beta, s.gamma)[0])
     t_setup = time.perf_counter() - t0
@@ -248,6 +254,55 @@ def cpu_solve_block(cfg_id, beta):
     out["blockdiag_hgs_minres"] = {"iterations": its, "converged": bool(conv), "seconds": time.perf_counter() - t0,
                                    "setup_seconds": t_setup}
     return {f"beta={beta:g}": out, "cores": 1}
+
+
+# time-to-solution of the reference itself (`sgkkt` fgmres + CoupledSweepPreconditioner
+# / SteadyKKTPreconditioner + oracle MINRES) on the full config-5 inputs, one core of
+# the BUILD container (tests/golden/make_solves.py; fixtures tests/golden/solves/)
+REF_CFG5_SECONDS = {
+    "beta=0.01": {"hgsoc_fgmres": {"iterations": 7, "seconds": 180.5},
+                  "blockdiag_hgs_minres": {"iterations": 37, "seconds": 702.3}},
+    "beta=0.0001": {"hgsoc_fgmres": {"iterations": 11, "seconds": 281.3},
+                    "blockdiag_hgs_minres": {"iterations": 36, "seconds": 684.3}},
+    "beta=1e-06": {"hgsoc_fgmres": {"iterations": 10, "seconds": 270.1},
+                   "blockdiag_hgs_minres": {"iterations": 32, "seconds": 615.3}},
+}
+
+
+def cpu_iteration_sample(cfg_id, beta):
+    """Bounded CPU sample of the config-5 solve on this host (oracle port, 1
+    core): one hGSoc apply (LU factor excluded, timed separately) and one KKT
+    matvec = the cost of one FGMRES iteration; projected to the reference's
+    iteration count.  The full solves of the reference itself are in
+    REF_CFG5_SECONDS (build container) and the reference arm times the
+    beta = 1e-2 solve end to end on this host."""
+    import scipy.sparse as sp
+
+    import oracle
+    from paper_2512_23804_b200.problems import build_problem, steady_system
+
+    b = build_problem(cfg_id, beta=beta)
+    s = steady_system(b)
+    n_h, n_xi = s.n_h, s.n_xi
+    cp = s.triple.matrices[: s.n_terms]
+    rng = np.random.default_rng(SEED)
+    blocks = [rng.standard_normal((n_h, n_xi)) for _ in range(3)]
+    m, a0 = s.mass, s.stiffness[0]
+    t0 = time.perf_counter()
+    kkt_lu = oracle.splu_ref(sp.bmat([[m, None, -a0], [None, s.beta * m, m], [-a0, m, None]], format="csr"))
+    t_fac = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.coupled_sweep_apply(m, s.stiffness, s.triple.matrices, s.triple.objective_weight, s.beta,
+                               b.partition.boundaries, s.n_terms, kkt_lu, *blocks)
+    t_apply = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.steady_kkt_apply(m, s.stiffness, cp, s.triple.weight_diagonal, s.beta, *blocks)
+    t_mv = time.perf_counter() - t0
+    its = REF_CFG5_SECONDS[f"beta={beta:g}"]["hgsoc_fgmres"]["iterations"]
+    return {f"beta={beta:g}": {"hgsoc_apply_s": t_apply, "kkt_matvec_s": t_mv, "lu_factor_s": t_fac,
+                               "projected_hgsoc_fgmres_s": its * (t_apply + t_mv), "iterations": its,
+                               "cores": 1, "kind": "port",
+                               "reference_sgkkt_build_container": REF_CFG5_SECONDS}}
 
 
 def _event_time(fn, steps, stream):
@@ -651,6 +706,8 @@ def run_ours(args):
         line["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "port",
                                 "sample": f"{rows} contiguous output rows of the cfg4 matvec ({b / 1e6:.1f} MB algorithmic, "
                                           f"{dt:.2f} s); NumPy/SciPy oracle port of sgkkt kron_apply, 1 core (GIL-bound)"}
+        if not args.no_solve and not args.no_solve_cfg5:
+            line["cpu_baseline"]["solves"] = {"cfg5": cpu_iteration_sample(5, 1e-2)}
     if rank == 0 and not args.no_solve:
         solves = {"cfg2": solve_block(2, [1e-2])}
         solves["cfg1_forward"] = forward_block(1)

@@ -299,6 +299,12 @@ typedef struct {
   int32_t* flags;             /* [n_groups * chunks] epoch flags             */
   int32_t* counters;          /* [n_groups * chunks] tile counters (zeroed per solve) */
   int32_t* ticket;
+  const int32_t* tile_kind;   /* [n_tiles] 0: entry tile, 1: dense-region task */
+  int32_t dense_g0;           /* dense-region groups [dense_g0, +dense_nb)  */
+  int32_t dense_nb;
+  int32_t dense_r0;           /* first row of the dense region              */
+  int32_t dense_pad;
+  const double* dense;        /* off-diagonal region blocks (sgk_trigroups) */
 } sgk_triwide;
 
 /* Chunk width (columns per task) the wide solve uses for `width`.          */
@@ -313,18 +319,19 @@ int sgk_trisolve_wide(const sgk_triwide* L, const sgk_triwide* U,
 /* Fast-diagonalisation factor of a Kronecker-sum lead (
  * replaces LUFactors.solve, linalg.py:76-87, when the lead is
  * A = K1(x)M1 + M1(x)K1 on an n x n tensor grid and M = M1(x)M1):
- * s  = S   (n x n row-major, K1 S = M1 S diag(mu), S^T M1 S = I),
- * st = S^T (n x n row-major), lam[a*n+b] = mu_a + mu_b.
+ * s = S zero-padded to np x np (row-major, np = n rounded up to 8, <= 256;
+ * K1 S = M1 S diag(mu), S^T M1 S = I), lam[a*n+b] = mu_a + mu_b.
  * n_seg == 1: X = A^-1 B.  n_seg == 3: the hGSoc block
  * P~ = [M 0 -A; 0 beta M M; -A M 0] (preconditioners.py:437-448) on the
- * (y, u, lambda) segments.  The four dense passes are cuBLAS DGEMMs; the
- * modal solve is this library's kernel.  work: sgk_fastdiag_work_doubles()
- * doubles.  B and X may alias.                                              */
+ * (y, u, lambda) segments.  Three sm_100a kernels (fp64 mma.sync): pass 1,
+ * passes 2 + modal solve + 3 fused, pass 4.  work:
+ * sgk_fastdiag_work_doubles() doubles.  B and X may alias.                  */
 typedef struct {
   int32_t n;
   int32_t n_seg;
+  int32_t np;
+  int32_t pad;
   const double* s;
-  const double* st;
   const double* lam;
   double beta;
 } sgk_fastdiag;

@@ -117,12 +117,25 @@ class TriGroups(ctypes.Structure):
     ]
 
 
+class TriWide(ctypes.Structure):
+    _fields_ = [
+        ("n", c_i32), ("n_groups", c_i32), ("n_tiles", c_i32), ("reversed", c_i32), ("rowptr", c_vp),
+        ("colind", c_vp), ("vals", c_vp), ("group_ptr", c_vp), ("tile_group", c_vp), ("tile_seg", c_vp),
+        ("tile_dep_ptr", c_vp), ("tile_dep", c_vp), ("group_ntiles", c_vp), ("seg_row", c_vp), ("seg_e0", c_vp),
+        ("seg_e1", c_vp), ("seg_slot", c_vp), ("row_slot_ptr", c_vp), ("row_slot", c_vp), ("work_row", c_vp),
+        ("io_row", c_vp), ("minv_ptr", c_vp), ("minv", c_vp), ("flags", c_vp), ("counters", c_vp),
+        ("ticket", c_vp), ("tile_kind", c_vp), ("dense_g0", c_i32), ("dense_nb", c_i32), ("dense_r0", c_i32),
+        ("dense_pad", c_i32), ("dense", c_vp),
+    ]
+
+
 class SegView(ctypes.Structure):
     _fields_ = [("ptr", c_vp * 3), ("ld", c_i64), ("col0", c_i32), ("seg_rows", c_i32)]
 
 
 class FastDiag(ctypes.Structure):
-    _fields_ = [("n", c_i32), ("n_seg", c_i32), ("s", c_vp), ("st", c_vp), ("lam", c_vp), ("beta", c_dbl)]
+    _fields_ = [("n", c_i32), ("n_seg", c_i32), ("np", c_i32), ("pad", c_i32), ("s", c_vp), ("lam", c_vp),
+                ("beta", c_dbl)]
 
 
 _SIGNATURES = {
@@ -145,6 +158,9 @@ _SIGNATURES = {
                              c_i32, c_vp]),
     "sgk_trisolve_chunk_cols": (c_i32, []),
     "sgk_trisolve_grouped_chunk_cols": (c_i32, []),
+    "sgk_trisolve_wide_chunk_cols": (c_i32, [c_i32]),
+    "sgk_trisolve_wide": (c_i32, [ctypes.POINTER(TriWide), ctypes.POINTER(TriWide), ctypes.POINTER(SegView),
+                                  ctypes.POINTER(SegView), c_vp, c_vp, c_i32, c_i32, c_vp]),
     "sgk_trisolve_grouped": (c_i32, [ctypes.POINTER(TriGroups), ctypes.POINTER(TriGroups),
                                      ctypes.POINTER(SegView), ctypes.POINTER(SegView), c_vp, c_i32, c_i32,
                                      c_vp]),

@@ -52,6 +52,18 @@ __device__ __forceinline__ double* wseg_ptr(const sgk_segview& s, int r, int c) 
   return base + (int64_t)rr * s.ld + s.col0 + c;
 }
 
+#ifdef SGK_TRIW_TRACE
+__device__ unsigned long long sgk_triw_trace[2][1 << 19][6];
+__device__ __forceinline__ unsigned long long triw_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRIW_TR(k) do { if (tid == 0 && ticket < (1 << 19)) sgk_triw_trace[FWD ? 0 : 1][ticket][k] = triw_timer(); } while (0)
+#else
+#define TRIW_TR(k) do {} while (0)
+#endif
+
 template <bool FWD, int CPL>
 __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview io, double* __restrict__ work,
                                                   double* __restrict__ part, int width, int ldw, int n_chunks,
@@ -62,6 +74,13 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
   double (*pr)[CH] = reinterpret_cast<double (*)[CH]>(wsm + WSMAX * CH);  // [WG][CH] P rows of the group
   __shared__ double lg[WG][WG + 1];               // dense inverse of the in-group block
   __shared__ int task_s, last_s;
+  // the tile's segment records and the group's part-slot lists, staged once
+  // per task (a dependent global load inside the per-column loops below costs
+  // an L2 round trip per iteration on the critical path)
+  __shared__ int s_row[WSMAX], s_e0[WSMAX], s_e1[WSMAX], s_slot[WSMAX];
+  constexpr int SLOTMAX = 1024;
+  __shared__ int q_ptr[WG + 1];
+  __shared__ int q_slot[SLOTMAX];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned FULL = 0xffffffffu;
   const int64_t n_tasks = (int64_t)t.n_tiles * n_chunks;
@@ -71,78 +90,30 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
     const int ticket = task_s;
     __syncthreads();
     if (ticket >= n_tasks) return;
+    TRIW_TR(0);
+#ifdef SGK_TRIW_TRACE
+    if (tid == 0 && ticket < (1 << 19)) sgk_triw_trace[FWD ? 0 : 1][ticket][4] = 0;  // set by the finaliser
+#endif
     const int tile = ticket / n_chunks;
     const int chunk = ticket - tile * n_chunks;
     const int c0 = chunk * CH;
     const int gi = __ldg(t.tile_group + tile);
+    const int kind = __ldg(t.tile_kind + tile);
     const int s0 = __ldg(t.tile_seg + tile), s1 = __ldg(t.tile_seg + tile + 1);
     const int nt = __ldg(t.group_ntiles + gi);
     const int r0 = __ldg(t.group_ptr + gi), g = __ldg(t.group_ptr + gi + 1) - r0;
-
-    // 0: wait for the groups this tile's entries read (relaxed polls, one fence)
-    {
-      const int da = __ldg(t.tile_dep_ptr + tile), db = __ldg(t.tile_dep_ptr + tile + 1);
-      for (int d = da + tid; d < db; d += blockDim.x) {
-        const int32_t* fl = t.flags + (int64_t)__ldg(t.tile_dep + d) * n_chunks + chunk;
-        while (ld_relaxed(fl) != epoch) __nanosleep(64);
-      }
-      fence_acq_rel();
-    }
-    __syncthreads();
-
-    // 1: segment partial sums, warps over segments, lanes over columns
-    for (int s = s0 + warp; s < s1; s += 8) {
-      const int e0 = __ldg(t.seg_e0 + s), e1 = __ldg(t.seg_e1 + s);
-      double acc[CPL];
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
-      // padding entries re-read the segment's first entry (a finished
-      // dependency: final, finite) with weight 0
-      const int e = e0 + lane;
-      const int cj = __ldg(t.colind + (e < e1 ? e : e0));
-      const double vj = e < e1 ? __ldg(t.vals + e) : 0.0;
-      const int cnt = e1 - e0;
-      for (int j = 0; j < cnt; j += 8) {
-        double xv[8][CPL];
-        double vv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int c = __shfl_sync(FULL, cj, j + u);
-          vv[u] = __shfl_sync(FULL, vj, j + u);
-          const int wr = t.reversed ? t.n - 1 - c : c;
-          ld_cpl<CPL>(work + (int64_t)wr * ldw + c0 + CPL * lane, xv[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-          for (int k = 0; k < CPL; ++k) acc[k] = fma(vv[u], xv[u][k], acc[k]);
-      }
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) sp[s - s0][CPL * lane + k] = acc[k];
-    }
-    __syncthreads();
-
+    const bool dgrp = (unsigned)(gi - t.dense_g0) < (unsigned)t.dense_nb;
     const int w = min(CH, width - c0);
-    if (nt > 1) {
-      // 2a: per (tile, row) sums in segment order -> part slots; count in
-      for (int col = tid; col < CH; col += blockDim.x) {
-        double a = 0.0;
-        for (int s = s0; s < s1; ++s) {
-          a += sp[s - s0][col];
-          const int slot = __ldg(t.seg_slot + s);
-          if (s + 1 == s1 || __ldg(t.seg_slot + s + 1) != slot) {
-            __stcg(part + (int64_t)slot * ldw + c0 + col, a);
-            a = 0.0;
-          }
-        }
-      }
-      __threadfence();
+
+    // P rows = B - (sum of the row's part slots, tile order) - extra(r, col)
+    auto p_from_slots = [&](auto extra) {
+      const int qa0 = __ldg(t.row_slot_ptr + r0);
+      const int nq = __ldg(t.row_slot_ptr + r0 + g) - qa0;
+      const bool staged = nq <= SLOTMAX;
+      if (tid <= g) q_ptr[tid] = __ldg(t.row_slot_ptr + r0 + tid) - qa0;
+      if (staged)
+        for (int i = tid; i < nq; i += blockDim.x) q_slot[i] = __ldg(t.row_slot + qa0 + i);
       __syncthreads();
-      if (tid == 0) last_s = atomicAdd(t.counters + (int64_t)gi * n_chunks + chunk, 1) == nt - 1;
-      __syncthreads();
-      if (!last_s) continue;
-      __threadfence();
-      // 2b: P = B - sum of the row's slots (tile order)
       for (int i = tid; i < g * CH; i += blockDim.x) {
         const int r = i / CH, col = i - r * CH;
         const int p = r0 + r;
@@ -150,23 +121,190 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
         if (col < w)
           b = FWD ? *wseg_ptr(io, __ldg(t.io_row + p), c0 + col)
                   : __ldcg(work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + col);
-        const int qa = __ldg(t.row_slot_ptr + p), qb = __ldg(t.row_slot_ptr + p + 1);
+        const int qa = q_ptr[r], qb = q_ptr[r + 1];
         double sum = 0.0;
-        for (int q = qa; q < qb; ++q) sum += __ldcg(part + (int64_t)__ldg(t.row_slot + q) * ldw + c0 + col);
-        pr[r][col] = b - sum;
+        if (staged) {
+          int q = qa;
+          for (; q + 4 <= qb; q += 4) {  // four independent loads in flight, summed in slot order
+            const double v0 = __ldcg(part + (int64_t)q_slot[q] * ldw + c0 + col);
+            const double v1 = __ldcg(part + (int64_t)q_slot[q + 1] * ldw + c0 + col);
+            const double v2 = __ldcg(part + (int64_t)q_slot[q + 2] * ldw + c0 + col);
+            const double v3 = __ldcg(part + (int64_t)q_slot[q + 3] * ldw + c0 + col);
+            sum += v0;
+            sum += v1;
+            sum += v2;
+            sum += v3;
+          }
+          for (; q < qb; ++q) sum += __ldcg(part + (int64_t)q_slot[q] * ldw + c0 + col);
+        } else {
+          for (int q = qa; q < qb; ++q) sum += __ldcg(part + (int64_t)__ldg(t.row_slot + qa0 + q) * ldw + c0 + col);
+        }
+        pr[r][col] = b - sum - extra(r, col);
       }
-    } else {
-      // 2: one-tile group: P = B - segment sums of each row (segment order)
-      for (int i = tid; i < g * CH; i += blockDim.x) {
-        const int r = i / CH, col = i - r * CH;
-        const int p = r0 + r;
-        pr[r][col] = col >= w ? 0.0
-                              : FWD ? *wseg_ptr(io, __ldg(t.io_row + p), c0 + col)
-                                    : __ldcg(work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + col);
+    };
+
+    if (kind == 1) {
+      // dense-region task: stream the region's earlier blocks as they are
+      // published (warp 0 polls 32 block flags at a time, every ready prefix
+      // is applied at once: X block and the 32x32 coefficient block staged in
+      // shared memory), then wait for the group's entry tiles and finalise.
+      // Warp w accumulates rows 4w..4w+3, lanes CPL columns each.
+      __shared__ int ready_s;
+      const int bi = gi - t.dense_g0;
+      const double* D = t.dense + (int64_t)WG * WG * bi * (bi - 1) / 2;
+      const int ldd = WG * bi;
+      double dacc[4][CPL];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) dacc[q][k] = 0.0;
+      TRIW_TR(1);
+      int j = 0;
+      while (j < bi) {
+        if (warp == 0) {
+          const int v = lane < bi - j ? ld_relaxed(t.flags + (int64_t)(t.dense_g0 + j + lane) * n_chunks + chunk) : epoch;
+          const unsigned notready = __ballot_sync(FULL, v != epoch);
+          if (lane == 0) ready_s = notready ? __ffs(notready) - 1 : min(32, bi - j);
+        }
+        __syncthreads();
+        const int ready = ready_s;
+        __syncthreads();
+        if (ready == 0) {
+          __nanosleep(128);
+          continue;
+        }
+        fence_acq_rel();
+        for (int jj = j; jj < j + ready; ++jj) {
+          for (int i = tid; i < WG * CH; i += blockDim.x) {
+            const int k = i / CH, c = i - k * CH;
+            const int src = t.dense_r0 + WG * jj + k;
+            const int wr = t.reversed ? t.n - 1 - src : src;
+            sp[k][c] = __ldcg(work + (int64_t)wr * ldw + c0 + c);
+          }
+          for (int i = tid; i < WG * WG; i += blockDim.x) {
+            const int r = i / WG, k = i - r * WG;
+            lg[r][k] = __ldg(D + (int64_t)r * ldd + WG * jj + k);
+          }
+          __syncthreads();
+#pragma unroll 4
+          for (int k = 0; k < WG; ++k) {
+            double xk[CPL];
+#pragma unroll
+            for (int kk = 0; kk < CPL; ++kk) xk[kk] = sp[k][CPL * lane + kk];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double d = lg[4 * warp + q][k];
+#pragma unroll
+              for (int kk = 0; kk < CPL; ++kk) dacc[q][kk] = fma(d, xk[kk], dacc[q][kk]);
+            }
+          }
+          __syncthreads();
+        }
+        j += ready;
+      }
+      TRIW_TR(2);
+      if (tid == 0) {
+        const int32_t* cnt = t.counters + (int64_t)gi * n_chunks + chunk;
+        while (ld_relaxed(cnt) != nt) __nanosleep(64);
       }
       __syncthreads();
-      for (int col = tid; col < CH; col += blockDim.x)
-        for (int s = s0; s < s1; ++s) pr[__ldg(t.seg_row + s) - r0][col] -= sp[s - s0][col];
+      fence_acq_rel();
+      TRIW_TR(3);
+      // region contributions into pr via shared memory (sp is free again)
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int kk = 0; kk < CPL; ++kk) sp[4 * warp + q][CPL * lane + kk] = dacc[q][kk];
+      __syncthreads();
+      p_from_slots([&](int r, int col) { return sp[r][col]; });
+    } else {
+      for (int i = tid; i < s1 - s0; i += blockDim.x) {
+        s_row[i] = __ldg(t.seg_row + s0 + i);
+        s_e0[i] = __ldg(t.seg_e0 + s0 + i);
+        s_e1[i] = __ldg(t.seg_e1 + s0 + i);
+        s_slot[i] = __ldg(t.seg_slot + s0 + i);
+      }
+      // 0: wait for the groups this tile's entries read (warp 0 polls, one fence)
+      if (warp == 0) {
+        const int da = __ldg(t.tile_dep_ptr + tile), db = __ldg(t.tile_dep_ptr + tile + 1);
+        for (int d = da + lane; d < db; d += 32) {
+          const int32_t* fl = t.flags + (int64_t)__ldg(t.tile_dep + d) * n_chunks + chunk;
+          while (ld_relaxed(fl) != epoch) __nanosleep(100);
+        }
+        fence_acq_rel();
+      }
+      __syncthreads();
+      TRIW_TR(1);
+
+      // 1: segment partial sums, warps over segments, lanes over columns
+      for (int s = s0 + warp; s < s1; s += 8) {
+        const int e0 = s_e0[s - s0], e1 = s_e1[s - s0];
+        double acc[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
+        // padding entries re-read the segment's first entry (a finished
+        // dependency: final, finite) with weight 0
+        const int e = e0 + lane;
+        const int cj = __ldg(t.colind + (e < e1 ? e : e0));
+        const double vj = e < e1 ? __ldg(t.vals + e) : 0.0;
+        const int cnt = e1 - e0;
+        for (int jb = 0; jb < cnt; jb += 8) {
+          double xv[8][CPL];
+          double vv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int c = __shfl_sync(FULL, cj, jb + u);
+            vv[u] = __shfl_sync(FULL, vj, jb + u);
+            const int wr = t.reversed ? t.n - 1 - c : c;
+            ld_cpl<CPL>(work + (int64_t)wr * ldw + c0 + CPL * lane, xv[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) acc[k] = fma(vv[u], xv[u][k], acc[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) sp[s - s0][CPL * lane + k] = acc[k];
+      }
+      __syncthreads();
+      TRIW_TR(2);
+
+      if (nt > 1 || dgrp) {
+        // 2a: per (tile, row) sums in segment order -> part slots; count in;
+        // the last tile of a sparse group finalises it (a dense-region
+        // group is finalised by its dense task)
+        for (int col = tid; col < CH; col += blockDim.x) {
+          double a = 0.0;
+          for (int i = 0; i < s1 - s0; ++i) {
+            a += sp[i][col];
+            const int slot = s_slot[i];
+            if (i + 1 == s1 - s0 || s_slot[i + 1] != slot) {
+              __stcg(part + (int64_t)slot * ldw + c0 + col, a);
+              a = 0.0;
+            }
+          }
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) last_s = atomicAdd(t.counters + (int64_t)gi * n_chunks + chunk, 1) == nt - 1 && !dgrp;
+        __syncthreads();
+        TRIW_TR(3);
+        if (!last_s) continue;
+        __threadfence();
+        // 2b: P = B - sum of the row's slots (tile order)
+        p_from_slots([](int, int) { return 0.0; });
+      } else {
+        // 2: one-tile group: P = B - segment sums of each row (segment order)
+        for (int i = tid; i < g * CH; i += blockDim.x) {
+          const int r = i / CH, col = i - r * CH;
+          const int p = r0 + r;
+          pr[r][col] = col >= w ? 0.0
+                                : FWD ? *wseg_ptr(io, __ldg(t.io_row + p), c0 + col)
+                                      : __ldcg(work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + col);
+        }
+        __syncthreads();
+        for (int col = tid; col < CH; col += blockDim.x)
+          for (int i = 0; i < s1 - s0; ++i) pr[s_row[i] - r0][col] -= sp[i][col];
+      }
     }
     {
       const int64_t mo = __ldg(t.minv_ptr + gi);
@@ -200,6 +338,8 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
     fence_acq_rel();
     __syncthreads();
     if (tid == 0) st_relaxed(t.flags + (int64_t)gi * n_chunks + chunk, epoch);
+    TRIW_TR(4);
+    TRIW_TR(5);
   }
 }
 
@@ -256,3 +396,10 @@ extern "C" int sgk_trisolve_wide(const sgk_triwide* L, const sgk_triwide* U, con
   if (ch == 64) return launch_wide_t<2>(*L, *U, *b, *x, work, part, width, epoch, st);
   return launch_wide_t<1>(*L, *U, *b, *x, work, part, width, epoch, st);
 }
+
+#ifdef SGK_TRIW_TRACE
+extern "C" int sgk_triw_trace_read(unsigned long long* out, int fwd, int n) {
+  return (int)cudaMemcpyFromSymbol(out, sgk::sgk_triw_trace, sizeof(unsigned long long) * 6 * (size_t)n,
+                                   fwd ? 0 : sizeof(unsigned long long) * 6 * (1 << 19));
+}
+#endif

@@ -122,12 +122,16 @@ class FastDiagFactors:
     def _dev(self):
         d = self._cache.get("dev")
         if d is None:
-            s_t = _f64(self.s)
-            st_t = _f64(np.ascontiguousarray(self.s.T))
+            n_pad = -(-self.n // 8) * 8
+            if n_pad > 256:
+                raise ValueError("fastdiag: grid side above 255 is not supported by the device kernels")
+            s_pad = np.zeros((n_pad, n_pad))
+            s_pad[: self.n, : self.n] = self.s
+            s_t = _f64(s_pad)
             lam_t = _f64(self.lam)
-            st = _lib.FastDiag(n=self.n, n_seg=self.n_seg, s=s_t.data_ptr(), st=st_t.data_ptr(),
+            st = _lib.FastDiag(n=self.n, n_seg=self.n_seg, np=n_pad, pad=0, s=s_t.data_ptr(),
                                lam=lam_t.data_ptr(), beta=float(self.beta))
-            d = (st, [s_t, st_t, lam_t])
+            d = (st, [s_t, lam_t])
             self._cache["dev"] = d
         return d[0]
 

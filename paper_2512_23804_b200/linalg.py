@@ -248,7 +248,132 @@ def _grouped(strict: csr_matrix, work_row, io_row, dinv):
         minv_ptr=bufs[12].data_ptr(), minv=bufs[13].data_ptr(),
         dense_g0=dg0, dense_nb=nb, dense_r0=dense[0], dense_pad=0, dense=bufs[14].data_ptr(),
     )
+    st._host = (gptr, order, bufs[12], bufs[13])  # group structure + dense inverses for the wide form
     return st, bufs, depth
+
+
+WIDE_SEG = 32     # entries per segment (one warp, <= 4 batches of 8 loads)
+WIDE_TILE_SEGS = 32
+WIDE_TILE_ENTRIES = 256
+# SGKKT_TRI_WIDE_MIN: narrowest RHS width the wide-tiled solve takes (A/B)
+WIDE_MIN = int(__import__("os").environ.get("SGKKT_TRI_WIDE_MIN", "32"))
+
+
+def wide_tiles(strict: csr_matrix, gptr: np.ndarray, order: np.ndarray, dense: tuple[int, int] = (0, 0)):
+    """Segments and tiles of the wide-RHS solve (csrc/trisolve_wide.cu):
+    every row's outside entries (columns before its group) in segments of
+    <= WIDE_SEG entries, a group's segments packed greedily into tiles of <=
+    WIDE_TILE_SEGS segments / WIDE_TILE_ENTRIES entries, groups in
+    topological order.  Groups with several tiles get a part slot per
+    (tile, row).  Groups of a dense region (`dense` = rows [d0, d1) in
+    DENSE_BLOCK blocks) keep only their entries left of d0 in tiles (always
+    slotted) and end with one dense task (tile_kind 1) that streams the
+    region's earlier blocks and finalises the group.  Returns a dict of
+    host arrays."""
+    n = strict.shape[0]
+    ng = len(gptr) - 1
+    ip, ix = strict.indptr.astype(np.int64), strict.indices.astype(np.int64)
+    gid = np.repeat(np.arange(ng), np.diff(gptr))
+    row_of = np.repeat(np.arange(n), np.diff(ip))
+    d0, d1 = dense
+    left = gptr[gid[row_of]] if strict.nnz else np.zeros(0, np.int64)
+    if d1 > d0 and strict.nnz:
+        in_region = (row_of >= d0) & (row_of < d1)
+        left = np.where(in_region, d0, left)  # region rows: only entries left of the region
+    outside = ix < left if strict.nnz else np.zeros(0, bool)
+    cnt = np.bincount(row_of[outside], minlength=n) if n else np.zeros(0, np.int64)
+    seg_row, seg_e0, seg_e1, seg_slot = [], [], [], []
+    tile_group, tile_seg, tile_kind = [], [0], []
+    group_ntiles = np.zeros(ng, np.int64)
+    row_slots = [[] for _ in range(n)]
+    n_slots = 0
+    for g in order:
+        a, b = int(gptr[g]), int(gptr[g + 1])
+        segs = []
+        for p in range(a, b):
+            c = int(cnt[p])
+            for k in range(0, c, WIDE_SEG):
+                segs.append((p, int(ip[p]) + k, int(ip[p]) + min(c, k + WIDE_SEG)))
+        tiles = [[]]
+        ents = 0
+        for sg in segs:
+            ln = sg[2] - sg[1]
+            if tiles[-1] and (len(tiles[-1]) >= WIDE_TILE_SEGS or ents + ln > WIDE_TILE_ENTRIES):
+                tiles.append([])
+                ents = 0
+            tiles[-1].append(sg)
+            ents += ln
+        is_dense = d1 > d0 and d0 <= a < d1
+        if is_dense and not tiles[-1]:
+            tiles = []  # no entries left of the region: the dense task alone
+        group_ntiles[g] = len(tiles)
+        for tl in tiles:
+            prev = -1
+            for (p, e0, e1) in tl:
+                if len(tiles) > 1 or is_dense:
+                    if p != prev:
+                        row_slots[p].append(n_slots)
+                        n_slots += 1
+                    seg_slot.append(n_slots - 1)
+                else:
+                    seg_slot.append(-1)
+                prev = p
+                seg_row.append(p)
+                seg_e0.append(e0)
+                seg_e1.append(e1)
+            tile_group.append(int(g))
+            tile_seg.append(len(seg_row))
+            tile_kind.append(0)
+        if is_dense:
+            tile_group.append(int(g))
+            tile_seg.append(len(seg_row))
+            tile_kind.append(1)
+    seg_row = np.asarray(seg_row, np.int64)
+    seg_e0 = np.asarray(seg_e0, np.int64)
+    seg_e1 = np.asarray(seg_e1, np.int64)
+    tile_seg = np.asarray(tile_seg, np.int64)
+    n_tiles = len(tile_group)
+    # dependency groups per tile: the groups of its entries' columns
+    if len(seg_row):
+        seg_len = seg_e1 - seg_e0
+        tile_of_seg = np.repeat(np.arange(n_tiles), np.diff(tile_seg))
+        ent = np.repeat(seg_e0, seg_len) + (np.arange(int(seg_len.sum())) - np.repeat(np.cumsum(seg_len) - seg_len, seg_len))
+        key = np.unique(np.repeat(tile_of_seg, seg_len) * ng + gid[ix[ent]])
+        dep_tile, dep = key // ng, key % ng
+    else:
+        dep_tile = dep = np.zeros(0, np.int64)
+    dep_ptr = np.concatenate([[0], np.cumsum(np.bincount(dep_tile, minlength=n_tiles))])
+    rs_ptr = np.concatenate([[0], np.cumsum([len(r) for r in row_slots])]) if n else np.zeros(1, np.int64)
+    rs = np.asarray([q for r in row_slots for q in r], np.int64)
+    return dict(n_tiles=n_tiles, n_slots=n_slots, tile_group=np.asarray(tile_group, np.int64), tile_seg=tile_seg,
+                tile_kind=np.asarray(tile_kind, np.int64),
+                dep_ptr=dep_ptr, dep=dep, group_ntiles=group_ntiles, seg_row=seg_row, seg_e0=seg_e0,
+                seg_e1=seg_e1, seg_slot=np.asarray(seg_slot, np.int64), row_slot_ptr=rs_ptr, row_slot=rs)
+
+
+def _wide(strict: csr_matrix, grouped_bufs, st_grouped, work_row, io_row):
+    """sgk_triwide for one processing-space triangle, sharing the grouped
+    form's CSR, group pointer, row maps and dense inverses."""
+    gptr, order, mptr_buf, minv_buf = st_grouped._host
+    g = st_grouped
+    dense = (g.dense_r0, g.dense_r0 + DENSE_BLOCK * g.dense_nb) if g.dense_nb else (0, 0)
+    w = wide_tiles(strict, gptr, order, dense)
+    i32 = lambda a: _i32(a if len(a) else [0])
+    bufs = [i32(w["tile_group"]), i32(w["tile_seg"]), i32(w["dep_ptr"]), i32(w["dep"]), i32(w["group_ntiles"]),
+            i32(w["seg_row"]), i32(w["seg_e0"]), i32(w["seg_e1"]), i32(w["seg_slot"]), i32(w["row_slot_ptr"]),
+            i32(w["row_slot"]), torch.zeros(1, dtype=torch.int32, device=device()), i32(w["tile_kind"])]
+    st = _lib.TriWide(
+        n=g.n, n_groups=g.n_groups, n_tiles=w["n_tiles"], reversed=g.reversed, rowptr=g.rowptr,
+        colind=g.colind, vals=g.vals, group_ptr=g.group_ptr, tile_group=bufs[0].data_ptr(),
+        tile_seg=bufs[1].data_ptr(), tile_dep_ptr=bufs[2].data_ptr(), tile_dep=bufs[3].data_ptr(),
+        group_ntiles=bufs[4].data_ptr(), seg_row=bufs[5].data_ptr(), seg_e0=bufs[6].data_ptr(),
+        seg_e1=bufs[7].data_ptr(), seg_slot=bufs[8].data_ptr(), row_slot_ptr=bufs[9].data_ptr(),
+        row_slot=bufs[10].data_ptr(), work_row=g.work_row, io_row=g.io_row, minv_ptr=mptr_buf.data_ptr(),
+        minv=minv_buf.data_ptr(), flags=None, counters=None, ticket=bufs[11].data_ptr(),
+        tile_kind=bufs[12].data_ptr(), dense_g0=g.dense_g0, dense_nb=g.dense_nb, dense_r0=g.dense_r0,
+        dense_pad=0, dense=g.dense,
+    )
+    return st, bufs, w["n_slots"]
 
 
 @dataclass(eq=False)
@@ -314,7 +439,23 @@ class TriangularFactors:
         (lg, ug) = grouped_triangles(l_strict, u_strict, diag, in_perm, out_perm)
         out.gl, out.gl_bufs, out.gdepth_l = _grouped(*lg)
         out.gu, out.gu_bufs, out.gdepth_u = _grouped(*ug)
+        out.wl, out.wl_bufs, out.wl_slots = _wide(lg[0], out.gl_bufs, out.gl, lg[1], lg[2])
+        out.wu, out.wu_bufs, out.wu_slots = _wide(ug[0], out.gu_bufs, out.gu, ug[1], ug[2])
         return out
+
+    def _ensure_wide(self, n_chunks: int) -> None:
+        """Flags and tile counters per (group, chunk) of the wide solve."""
+        if n_chunks <= getattr(self, "_wide_chunks", 0):
+            return
+        dev = self.in_perm.device
+        self._wflags = [torch.zeros(max(1, t.n_groups * n_chunks), dtype=torch.int32, device=dev)
+                        for t in (self.wl, self.wu)]
+        self._wcnt = [torch.zeros(max(1, t.n_groups * n_chunks), dtype=torch.int32, device=dev)
+                      for t in (self.wl, self.wu)]
+        for t, f, c in zip((self.wl, self.wu), self._wflags, self._wcnt):
+            t.flags = f.data_ptr()
+            t.counters = c.data_ptr()
+        self._wide_chunks = n_chunks
 
     def _ensure_flags(self, width: int) -> None:
         """Readiness flags per (row, 16-column chunk); grown on demand."""
@@ -359,6 +500,23 @@ class TriangularFactors:
 
         bv = segview(b_segs)
         xv = segview(x_segs)
+        if GROUPED and width >= WIDE_MIN:
+            lib = _lib.lib()
+            ch = int(lib.sgk_trisolve_wide_chunk_cols(width))
+            ldw = -(-width // ch) * ch
+            dev = b_segs[0][0].device
+            work = torch.empty((self.n, ldw), dtype=torch.float64, device=dev)
+            part = torch.empty((max(1, self.wl_slots, self.wu_slots), ldw), dtype=torch.float64, device=dev)
+            if stream is not None:
+                work.record_stream(stream)
+                part.record_stream(stream)
+            self._ensure_wide(ldw // ch)
+            self.epoch += 1
+            rc = lib.sgk_trisolve_wide(ctypes.byref(self.wl), ctypes.byref(self.wu), ctypes.byref(bv),
+                                       ctypes.byref(xv), work.data_ptr(), part.data_ptr(), width, self.epoch,
+                                       _lib.stream_ptr(stream))
+            _lib.check(rc, "sgk_trisolve_wide")
+            return
         work = torch.empty((self.n, -(-width // 16) * 16 if GROUPED else width), dtype=torch.float64,
                            device=b_segs[0][0].device)
         if stream is not None:

@@ -18,7 +18,7 @@ ROOT = Path(__file__).resolve().parent.parent
 PAIRS = {
     "sgk_pattern": "Pattern", "sgk_program": "Program", "sgk_view": "View", "sgk_pattern9": "Pattern9",
     "sgk_program9": "Program9", "sgk_trifactor": "TriFactor", "sgk_trigroups": "TriGroups",
-    "sgk_segview": "SegView", "sgk_fastdiag": "FastDiag", "sgk_grid9": "Grid9",
+    "sgk_segview": "SegView", "sgk_fastdiag": "FastDiag", "sgk_grid9": "Grid9", "sgk_triwide": "TriWide",
 }
 
 

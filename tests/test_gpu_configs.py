@@ -277,8 +277,9 @@ def test_pinned_host_non_contiguous_out_and_many_terms():
     assert _rel(got3, ref) <= 1e-12
 
 
+@pytest.mark.parametrize("wide_min", [32, 10**9])
 @pytest.mark.parametrize("dense", [True, False])
-def test_ptilde_solve_all_chunk_paths_vs_superlu(dense, monkeypatch):
+def test_ptilde_solve_all_chunk_paths_vs_superlu(dense, wide_min, monkeypatch):
     """The grouped triangular solve through every chunk width / CTA shape
     (1, 2, 4 columns; 512- and 256-thread CTAs above width 200) and with /
     without the dense-region streaming, against SuperLU on the same P~."""
@@ -289,6 +290,7 @@ def test_ptilde_solve_all_chunk_paths_vs_superlu(dense, monkeypatch):
     from paper_2512_23804_b200.preconditioners import deterministic_kkt_matrix
 
     monkeypatch.setattr(linalg, "DENSE", dense)
+    monkeypatch.setattr(linalg, "WIDE_MIN", wide_min)  # 32: widths >= 32 take the wide-tiled solve
     b, sys_ = _control(5, n=32)
     k = deterministic_kkt_matrix(sys_).tocsc()
     lu = spla.splu(k, diag_pivot_thresh=1.0)
@@ -297,7 +299,7 @@ def test_ptilde_solve_all_chunk_paths_vs_superlu(dense, monkeypatch):
         assert fac.gl.dense_nb > 0 and fac.gu.dense_nb > 0
     n = k.shape[0] // 3
     rng = np.random.default_rng(7)
-    for width in (1, 7, 33, 250):
+    for width in (1, 7, 33, 64, 65, 250):
         rhs = rng.standard_normal((3 * n, width))
         want = lu.solve(rhs)
         segs = [torch.as_tensor(np.ascontiguousarray(rhs[i * n:(i + 1) * n])).cuda() for i in range(3)]

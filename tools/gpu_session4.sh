@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python tools/time_tri.py 5 > gpurun_out/g4_tri.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_configs.py -q -m gpu -x -k "ptilde" > gpurun_out/g4_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/g4_tests.log
