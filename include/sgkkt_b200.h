@@ -334,6 +334,13 @@ typedef struct {
   const double* s;
   const double* lam;
   double beta;
+  /* centrosymmetric form (NULL sh: full passes): modes ordered symmetric
+   * first (ne of them, lam and s permuted alike); sh = S_E = S[0:h+n%2, 0:ne]
+   * then S_O = S[0:h, ne:n], each zero-padded to hp x hp (h = n/2, hp = a
+   * multiple of 8 >= h+1, <= 128): half-size GEMMs around a butterfly.    */
+  int32_t ne;
+  int32_t hp;
+  const double* sh;
 } sgk_fastdiag;
 int64_t sgk_fastdiag_work_doubles(const sgk_fastdiag* fd, int32_t width);
 int sgk_fastdiag_solve(const sgk_fastdiag* fd, const sgk_segview* b,

@@ -135,7 +135,7 @@ class SegView(ctypes.Structure):
 
 class FastDiag(ctypes.Structure):
     _fields_ = [("n", c_i32), ("n_seg", c_i32), ("np", c_i32), ("pad", c_i32), ("s", c_vp), ("lam", c_vp),
-                ("beta", c_dbl)]
+                ("beta", c_dbl), ("ne", c_i32), ("hp", c_i32), ("sh", c_vp)]
 
 
 _SIGNATURES = {

@@ -30,6 +30,8 @@ namespace sgk {
 
 constexpr int WG = 32;     // rows per group (= GMAX of trisolve.cu, linalg.GROUP_MAX)
 constexpr int WSMAX = 32;  // segments per tile
+constexpr int WW = 16;     // warps per CTA
+constexpr int WB = 16;     // entries per batch (loads in flight per warp)
 
 template <int CPL>
 __device__ __forceinline__ void ld_cpl(const double* __restrict__ p, double (&x)[CPL]) {
@@ -65,14 +67,15 @@ __device__ __forceinline__ unsigned long long triw_timer() {
 #endif
 
 template <bool FWD, int CPL>
-__global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview io, double* __restrict__ work,
+__global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview io, double* __restrict__ work,
                                                   double* __restrict__ part, int width, int ldw, int n_chunks,
                                                   int epoch) {
   constexpr int CH = 32 * CPL;
   extern __shared__ __align__(16) double wsm[];
   double (*sp)[CH] = reinterpret_cast<double (*)[CH]>(wsm);               // [WSMAX][CH] segment partials
   double (*pr)[CH] = reinterpret_cast<double (*)[CH]>(wsm + WSMAX * CH);  // [WG][CH] P rows of the group
-  __shared__ double lg[WG][WG + 1];               // dense inverse of the in-group block
+  __shared__ double lg[WG][WG + 1];               // dense-region coefficient block (dense task)
+  __shared__ double mv[WG][WG + 1];               // dense inverse of the in-group block
   __shared__ int task_s, last_s;
   // the tile's segment records and the group's part-slot lists, staged once
   // per task (a dependent global load inside the per-column loops below costs
@@ -104,6 +107,17 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
     const int r0 = __ldg(t.group_ptr + gi), g = __ldg(t.group_ptr + gi + 1) - r0;
     const bool dgrp = (unsigned)(gi - t.dense_g0) < (unsigned)t.dense_nb;
     const int w = min(CH, width - c0);
+    // the group's dense inverse is static: tasks that always finalise load it
+    // up front (its latency overlaps the dependency wait / the streaming)
+    auto load_minv = [&]() {
+      const int64_t mo = __ldg(t.minv_ptr + gi);
+      for (int i = tid; i < g * g; i += blockDim.x) {
+        const int r = i / g, k = i - r * g;
+        mv[r][k] = __ldg(t.minv + mo + i);
+      }
+    };
+    const bool minv_early = kind == 1 || (nt == 1 && !dgrp);
+    if (minv_early) load_minv();
 
     // P rows = B - (sum of the row's part slots, tile order) - extra(r, col)
     auto p_from_slots = [&](auto extra) {
@@ -148,14 +162,14 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
       // published (warp 0 polls 32 block flags at a time, every ready prefix
       // is applied at once: X block and the 32x32 coefficient block staged in
       // shared memory), then wait for the group's entry tiles and finalise.
-      // Warp w accumulates rows 4w..4w+3, lanes CPL columns each.
+      // Warp w accumulates rows 2w, 2w+1, lanes CPL columns each.
       __shared__ int ready_s;
       const int bi = gi - t.dense_g0;
       const double* D = t.dense + (int64_t)WG * WG * bi * (bi - 1) / 2;
       const int ldd = WG * bi;
-      double dacc[4][CPL];
+      double dacc[2][CPL];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 2; ++q)
 #pragma unroll
         for (int k = 0; k < CPL; ++k) dacc[q][k] = 0.0;
       TRIW_TR(1);
@@ -170,7 +184,7 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
         const int ready = ready_s;
         __syncthreads();
         if (ready == 0) {
-          __nanosleep(128);
+          __nanosleep(32);
           continue;
         }
         fence_acq_rel();
@@ -192,8 +206,8 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
 #pragma unroll
             for (int kk = 0; kk < CPL; ++kk) xk[kk] = sp[k][CPL * lane + kk];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const double d = lg[4 * warp + q][k];
+            for (int q = 0; q < 2; ++q) {
+              const double d = lg[2 * warp + q][k];
 #pragma unroll
               for (int kk = 0; kk < CPL; ++kk) dacc[q][kk] = fma(d, xk[kk], dacc[q][kk]);
             }
@@ -211,9 +225,9 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
       fence_acq_rel();
       TRIW_TR(3);
       // region contributions into pr via shared memory (sp is free again)
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 2; ++q)
 #pragma unroll
-        for (int kk = 0; kk < CPL; ++kk) sp[4 * warp + q][CPL * lane + kk] = dacc[q][kk];
+        for (int kk = 0; kk < CPL; ++kk) sp[2 * warp + q][CPL * lane + kk] = dacc[q][kk];
       __syncthreads();
       p_from_slots([&](int r, int col) { return sp[r][col]; });
     } else {
@@ -228,7 +242,7 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
         const int da = __ldg(t.tile_dep_ptr + tile), db = __ldg(t.tile_dep_ptr + tile + 1);
         for (int d = da + lane; d < db; d += 32) {
           const int32_t* fl = t.flags + (int64_t)__ldg(t.tile_dep + d) * n_chunks + chunk;
-          while (ld_relaxed(fl) != epoch) __nanosleep(100);
+          while (ld_relaxed(fl) != epoch) __nanosleep(32);
         }
         fence_acq_rel();
       }
@@ -236,7 +250,7 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
       TRIW_TR(1);
 
       // 1: segment partial sums, warps over segments, lanes over columns
-      for (int s = s0 + warp; s < s1; s += 8) {
+      for (int s = s0 + warp; s < s1; s += WW) {
         const int e0 = s_e0[s - s0], e1 = s_e1[s - s0];
         double acc[CPL];
 #pragma unroll
@@ -247,18 +261,18 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
         const int cj = __ldg(t.colind + (e < e1 ? e : e0));
         const double vj = e < e1 ? __ldg(t.vals + e) : 0.0;
         const int cnt = e1 - e0;
-        for (int jb = 0; jb < cnt; jb += 8) {
-          double xv[8][CPL];
-          double vv[8];
+        for (int jb = 0; jb < cnt; jb += WB) {
+          double xv[WB][CPL];
+          double vv[WB];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < WB; ++u) {
             const int c = __shfl_sync(FULL, cj, jb + u);
             vv[u] = __shfl_sync(FULL, vj, jb + u);
             const int wr = t.reversed ? t.n - 1 - c : c;
             ld_cpl<CPL>(work + (int64_t)wr * ldw + c0 + CPL * lane, xv[u]);
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < WB; ++u)
 #pragma unroll
             for (int k = 0; k < CPL; ++k) acc[k] = fma(vv[u], xv[u][k], acc[k]);
         }
@@ -306,23 +320,17 @@ __global__ void __launch_bounds__(256, 2) trsv_wide(sgk_triwide t, sgk_segview i
           for (int i = 0; i < s1 - s0; ++i) pr[s_row[i] - r0][col] -= sp[i][col];
       }
     }
-    {
-      const int64_t mo = __ldg(t.minv_ptr + gi);
-      for (int i = tid; i < g * g; i += blockDim.x) {
-        const int r = i / g, k = i - r * g;
-        lg[r][k] = __ldg(t.minv + mo + i);
-      }
-    }
+    if (!minv_early) load_minv();
     __syncthreads();
 
     // 3: X = inv(D + B_g) P (lower triangular), rows over warps; write,
     //    fence, publish
-    for (int r = warp; r < g; r += 8) {
+    for (int r = warp; r < g; r += WW) {
       double acc[CPL];
 #pragma unroll
       for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
       for (int j = 0; j <= r; ++j) {
-        const double m = lg[r][j];
+        const double m = mv[r][j];
 #pragma unroll
         for (int k = 0; k < CPL; ++k) acc[k] = fma(m, pr[j][CPL * lane + k], acc[k]);
       }
@@ -358,7 +366,7 @@ static int launch_wide_t(const sgk_triwide& L, const sgk_triwide& U, const sgk_s
     attr_set = true;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_wide<true, CPL>, 256, dyn);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_wide<true, CPL>, 32 * WW, dyn);
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)sm_count() * occ;
   const int64_t tasks = (int64_t)std::max(L.n_tiles, U.n_tiles) * n_chunks;
@@ -368,16 +376,21 @@ static int launch_wide_t(const sgk_triwide& L, const sgk_triwide& U, const sgk_s
   cudaMemsetAsync(U.ticket, 0, sizeof(int32_t), st);
   cudaMemsetAsync(L.counters, 0, sizeof(int32_t) * (size_t)L.n_groups * n_chunks, st);
   cudaMemsetAsync(U.counters, 0, sizeof(int32_t) * (size_t)U.n_groups * n_chunks, st);
-  trsv_wide<true, CPL><<<(int)grid, 256, dyn, st>>>(L, b, work, part, width, ldw, n_chunks, epoch);
+  trsv_wide<true, CPL><<<(int)grid, 32 * WW, dyn, st>>>(L, b, work, part, width, ldw, n_chunks, epoch);
   int rc = check_launch("trsv_wide<fwd>");
   if (rc) return rc;
-  trsv_wide<false, CPL><<<(int)grid, 256, dyn, st>>>(U, x, work, part, width, ldw, n_chunks, epoch);
+  trsv_wide<false, CPL><<<(int)grid, 32 * WW, dyn, st>>>(U, x, work, part, width, ldw, n_chunks, epoch);
   return check_launch("trsv_wide<bwd>");
 }
 
 }  // namespace sgk
 
-extern "C" int32_t sgk_trisolve_wide_chunk_cols(int32_t width) { return width > 64 ? 128 : (width > 32 ? 64 : 32); }
+extern "C" int32_t sgk_trisolve_wide_chunk_cols(int32_t width) {
+  // 32-column chunks: every entry's solution-row load is one 256-byte read,
+  // and a level's group finalisations spread over width/32 CTAs; above 128
+  // columns 64-column chunks halve the task count (measured, cfg5 P~)
+  return width > 128 ? 64 : 32;
+}
 
 extern "C" int sgk_trisolve_wide(const sgk_triwide* L, const sgk_triwide* U, const sgk_segview* b,
                                  const sgk_segview* x, double* work, double* part, int32_t width, int32_t epoch,

@@ -53,6 +53,8 @@ __all__ = [
 ]
 
 KRON_TOL = 1e-12
+# SGKKT_FD_HALF=0 keeps the full-size passes for centrosymmetric leads (A/B)
+HALF = __import__("os").environ.get("SGKKT_FD_HALF", "1") != "0"
 
 
 def _grid_side(n_rows: int) -> int:
@@ -112,6 +114,7 @@ class FastDiagFactors:
     beta: float
     s: np.ndarray  # S (n x n), K1 S = M1 S diag(mu), S^T M1 S = I
     lam: np.ndarray  # mu_a + mu_b, a-major (n*n)
+    ne: int = -1  # symmetric modes first (centrosymmetric butterfly form), -1: full passes
     _cache: dict = field(default_factory=dict, repr=False, compare=False)
 
     # the factor is its own device object (same seam as TriangularFactors)
@@ -129,9 +132,21 @@ class FastDiagFactors:
             s_pad[: self.n, : self.n] = self.s
             s_t = _f64(s_pad)
             lam_t = _f64(self.lam)
+            keep = [s_t, lam_t]
+            ne, hp, sh = 0, 0, None
+            h = self.n // 2
+            if self.ne >= 0 and HALF and -(-(h + 1) // 8) * 8 <= 128:
+                ne = self.ne
+                hp = -(-(h + 1) // 8) * 8
+                halves = np.zeros((2, hp, hp))
+                halves[0, : h + self.n % 2, :ne] = self.s[: h + self.n % 2, :ne]
+                halves[1, :h, : self.n - ne] = self.s[:h, ne:]
+                sh_t = _f64(halves)
+                keep.append(sh_t)
+                sh = sh_t.data_ptr()
             st = _lib.FastDiag(n=self.n, n_seg=self.n_seg, np=n_pad, pad=0, s=s_t.data_ptr(),
-                               lam=lam_t.data_ptr(), beta=float(self.beta))
-            d = (st, [s_t, lam_t])
+                               lam=lam_t.data_ptr(), beta=float(self.beta), ne=ne, hp=hp, sh=sh)
+            d = (st, keep)
             self._cache["dev"] = d
         return d[0]
 
@@ -196,21 +211,45 @@ class FastDiagFactors:
         return out
 
 
+CENTRO_TOL = 1e-10  # eigh leaves ~1e-12 asymmetry in the A_1 modes (n = 127)
+
+
+def _centro_order(s: np.ndarray):
+    """Mode order for the centrosymmetric (butterfly) kernels: when every
+    1-D mode is symmetric or antisymmetric (S[n-1-i, j] = +-S[i, j] to
+    CENTRO_TOL relative — true for the symmetric Toeplitz K1, M1 of a
+    uniform grid), the permutation putting the symmetric modes first and
+    their count; else None (full passes)."""
+    n = s.shape[0]
+    flip = s[::-1, :]
+    norm = np.linalg.norm(s, axis=0)
+    par = np.sign(np.einsum("ij,ij->j", flip, s))
+    if np.any(par == 0) or np.max(np.linalg.norm(flip - par[None, :] * s, axis=0) / norm) > CENTRO_TOL:
+        return None
+    perm = np.concatenate([np.nonzero(par > 0)[0], np.nonzero(par < 0)[0]])
+    return perm, int(np.sum(par > 0))
+
+
 def _modal(a, mass):
     k1, m1 = kron_sum_split(a, mass)
     mu, s = scipy.linalg.eigh(k1, m1)
     n = len(mu)
+    ne = -1
+    co = _centro_order(s)
+    if co is not None:
+        perm, ne = co
+        s, mu = s[:, perm], mu[perm]
     lam = (mu[:, None] + mu[None, :]).reshape(-1)
-    return n, np.ascontiguousarray(s), np.ascontiguousarray(lam)
+    return n, np.ascontiguousarray(s), np.ascontiguousarray(lam), ne
 
 
 def fastdiag_factor(a: sp.spmatrix, mass: sp.spmatrix) -> FastDiagFactors:
     """Factor of a Kronecker-sum lead (A_1, or A_1 + c M): drop-in for
     sparse_lu(a) in the hGS lead slot (preconditioners.py:211-224)."""
-    n, s, lam = _modal(a, mass)
+    n, s, lam, ne = _modal(a, mass)
     if np.any(lam <= 0.0):
         raise ValueError("lead is not positive definite")
-    return FastDiagFactors(shape=a.shape, n=n, n_seg=1, beta=0.0, s=s, lam=lam)
+    return FastDiagFactors(shape=a.shape, n=n, n_seg=1, beta=0.0, s=s, lam=lam, ne=ne)
 
 
 def fastdiag_kkt_factor(a1: sp.spmatrix, mass: sp.spmatrix, beta: float) -> FastDiagFactors:
@@ -218,6 +257,6 @@ def fastdiag_kkt_factor(a1: sp.spmatrix, mass: sp.spmatrix, beta: float) -> Fast
     sparse_lu(deterministic_kkt_matrix(sys)) (preconditioners.py:451-462)."""
     if not beta > 0.0:
         raise ValueError("beta must be positive")
-    n, s, lam = _modal(a1, mass)
+    n, s, lam, ne = _modal(a1, mass)
     rows = 3 * n * n
-    return FastDiagFactors(shape=(rows, rows), n=n, n_seg=3, beta=float(beta), s=s, lam=lam)
+    return FastDiagFactors(shape=(rows, rows), n=n, n_seg=3, beta=float(beta), s=s, lam=lam, ne=ne)

@@ -55,9 +55,9 @@ for fwd, tw, bufs in ((1, fac.wl, fac.wl_bufs), (0, fac.wu, fac.wu_bufs)):
     print("   group finish (us) at deciles of the topological order:", np.round(fins[q], 0))
     # time from deps ready to segments done, per tile size (entries)
     e0 = bufs[6].cpu().numpy(); e1 = bufs[7].cpu().numpy(); ts = bufs[1].cpu().numpy()
-    ent = np.add.reduceat(e1 - e0, ts[:-1]) if len(e0) else np.zeros(tw.n_tiles)
-    ent = np.where(np.diff(ts) > 0, ent, 0)[tile]
-    for lo, hi in ((0, 64), (64, 200), (200, 300)):
+    cs = np.concatenate([[0], np.cumsum(e1 - e0)])
+    ent = (cs[ts[1:]] - cs[ts[:-1]])[tile]
+    for lo, hi in ((0, 128), (128, 512), (512, 1025)):
         sel = (ent >= lo) & (ent < hi)
         if sel.any():
             print(f"   tiles with {lo}-{hi} entries: {sel.sum()}, segments phase median {np.median(tr[sel, 2] - tr[sel, 1]):.2f} us")
