@@ -157,6 +157,16 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
       }
     };
 
+    // P rows = B (the right-hand side rows of the group; static)
+    auto init_b = [&]() {
+      for (int i = tid; i < g * CH; i += blockDim.x) {
+        const int r = i / CH, col = i - r * CH;
+        const int p = r0 + r;
+        pr[r][col] = col >= w ? 0.0
+                              : FWD ? *wseg_ptr(io, __ldg(t.io_row + p), c0 + col)
+                                    : __ldcg(work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + col);
+      }
+    };
     if (kind == 1) {
       // dense-region task: stream the region's earlier blocks as they are
       // published (warp 0 polls 32 block flags at a time, every ready prefix
@@ -173,7 +183,8 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
 #pragma unroll
         for (int k = 0; k < CPL; ++k) dacc[q][k] = 0.0;
       TRIW_TR(1);
-      int j = 0;
+      init_b();  // static: off the critical path (the streaming below waits anyway)
+      int j = 0, d_pref = -1;
       while (j < bi) {
         if (warp == 0) {
           const int v = lane < bi - j ? ld_relaxed(t.flags + (int64_t)(t.dense_g0 + j + lane) * n_chunks + chunk) : epoch;
@@ -184,6 +195,13 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         const int ready = ready_s;
         __syncthreads();
         if (ready == 0) {
+          if (d_pref != j) {  // the awaited block's coefficients are static: stage them while waiting
+            for (int i = tid; i < WG * WG; i += blockDim.x) {
+              const int r = i / WG, k = i - r * WG;
+              lg[r][k] = __ldg(D + (int64_t)r * ldd + WG * j + k);
+            }
+            d_pref = j;
+          }
           __nanosleep(32);
           continue;
         }
@@ -195,10 +213,12 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
             const int wr = t.reversed ? t.n - 1 - src : src;
             sp[k][c] = __ldcg(work + (int64_t)wr * ldw + c0 + c);
           }
-          for (int i = tid; i < WG * WG; i += blockDim.x) {
-            const int r = i / WG, k = i - r * WG;
-            lg[r][k] = __ldg(D + (int64_t)r * ldd + WG * jj + k);
-          }
+          if (d_pref != jj)
+            for (int i = tid; i < WG * WG; i += blockDim.x) {
+              const int r = i / WG, k = i - r * WG;
+              lg[r][k] = __ldg(D + (int64_t)r * ldd + WG * jj + k);
+            }
+          d_pref = -1;
           __syncthreads();
 #pragma unroll 4
           for (int k = 0; k < WG; ++k) {
@@ -217,19 +237,27 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         j += ready;
       }
       TRIW_TR(2);
-      if (tid == 0) {
-        const int32_t* cnt = t.counters + (int64_t)gi * n_chunks + chunk;
-        while (ld_relaxed(cnt) != nt) __nanosleep(64);
-      }
-      __syncthreads();
-      fence_acq_rel();
-      TRIW_TR(3);
-      // region contributions into pr via shared memory (sp is free again)
-      for (int q = 0; q < 2; ++q)
+      if (nt > 0) {
+        if (tid == 0) {
+          const int32_t* cnt = t.counters + (int64_t)gi * n_chunks + chunk;
+          while (ld_relaxed(cnt) != nt) __nanosleep(32);
+        }
+        __syncthreads();
+        fence_acq_rel();
+        TRIW_TR(3);
+        // region contributions into pr via shared memory (sp is free again)
+        for (int q = 0; q < 2; ++q)
 #pragma unroll
-        for (int kk = 0; kk < CPL; ++kk) sp[2 * warp + q][CPL * lane + kk] = dacc[q][kk];
-      __syncthreads();
-      p_from_slots([&](int r, int col) { return sp[r][col]; });
+          for (int kk = 0; kk < CPL; ++kk) sp[2 * warp + q][CPL * lane + kk] = dacc[q][kk];
+        __syncthreads();
+        p_from_slots([&](int r, int col) { return sp[r][col]; });
+      } else {
+        // no entries left of the region: P = B (prefetched) - region sum
+        __syncthreads();  // init_b's writes (bi == 0 has no streaming barrier)
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int kk = 0; kk < CPL; ++kk) pr[2 * warp + q][CPL * lane + kk] -= dacc[q][kk];
+      }
     } else {
       for (int i = tid; i < s1 - s0; i += blockDim.x) {
         s_row[i] = __ldg(t.seg_row + s0 + i);
