@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
   double (*pr)[CH] = reinterpret_cast<double (*)[CH]>(wsm + WSMAX * CH);  // [WG][CH] P rows of the group
   __shared__ double lg[WG][WG + 1];               // dense-region coefficient block (dense task)
   __shared__ double mv[WG][WG + 1];               // dense inverse of the in-group block
-  __shared__ int task_s, last_s;
+  __shared__ int task_s;
   // the tile's segment records and the group's part-slot lists, staged once
   // per task (a dependent global load inside the per-column loops below costs
   // an L2 round trip per iteration on the critical path)
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         mv[r][k] = __ldg(t.minv + mo + i);
       }
     };
-    const bool minv_early = kind == 1 || (nt == 1 && !dgrp);
+    const bool minv_early = kind != 0 || (nt == 1 && !dgrp);
     if (minv_early) load_minv();
 
     // P rows = B - (sum of the row's part slots, tile order) - extra(r, col)
@@ -157,6 +157,39 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
       }
     };
 
+    // P rows -= sum of the row's part slots (tile order)
+    auto sub_slots = [&]() {
+      const int qa0 = __ldg(t.row_slot_ptr + r0);
+      const int nq = __ldg(t.row_slot_ptr + r0 + g) - qa0;
+      const bool staged = nq <= SLOTMAX;
+      if (tid <= g) q_ptr[tid] = __ldg(t.row_slot_ptr + r0 + tid) - qa0;
+      if (staged)
+        for (int i = tid; i < nq; i += blockDim.x) q_slot[i] = __ldg(t.row_slot + qa0 + i);
+      __syncthreads();
+      for (int i = tid; i < g * CH; i += blockDim.x) {
+        const int r = i / CH, col = i - r * CH;
+        const int qa = q_ptr[r], qb = q_ptr[r + 1];
+        double sum = 0.0;
+        int q = qa;
+        for (; q + 4 <= qb; q += 4) {
+          const int sa = staged ? q_slot[q] : __ldg(t.row_slot + qa0 + q);
+          const int sb = staged ? q_slot[q + 1] : __ldg(t.row_slot + qa0 + q + 1);
+          const int sc = staged ? q_slot[q + 2] : __ldg(t.row_slot + qa0 + q + 2);
+          const int sd = staged ? q_slot[q + 3] : __ldg(t.row_slot + qa0 + q + 3);
+          const double v0 = __ldcg(part + (int64_t)sa * ldw + c0 + col);
+          const double v1 = __ldcg(part + (int64_t)sb * ldw + c0 + col);
+          const double v2 = __ldcg(part + (int64_t)sc * ldw + c0 + col);
+          const double v3 = __ldcg(part + (int64_t)sd * ldw + c0 + col);
+          sum += v0;
+          sum += v1;
+          sum += v2;
+          sum += v3;
+        }
+        for (; q < qb; ++q)
+          sum += __ldcg(part + (int64_t)(staged ? q_slot[q] : __ldg(t.row_slot + qa0 + q)) * ldw + c0 + col);
+        pr[r][col] -= sum;
+      }
+    };
     // P rows = B (the right-hand side rows of the group; static)
     auto init_b = [&]() {
       for (int i = tid; i < g * CH; i += blockDim.x) {
@@ -259,6 +292,9 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
           for (int kk = 0; kk < CPL; ++kk) pr[2 * warp + q][CPL * lane + kk] -= dacc[q][kk];
       }
     } else {
+      // tasks that always finalise load their group's B rows up front (static)
+      const bool b_early = kind == 2 || (nt == 1 && !dgrp);
+      if (b_early) init_b();
       for (int i = tid; i < s1 - s0; i += blockDim.x) {
         s_row[i] = __ldg(t.seg_row + s0 + i);
         s_e0[i] = __ldg(t.seg_e0 + s0 + i);
@@ -310,10 +346,23 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
       __syncthreads();
       TRIW_TR(2);
 
-      if (nt > 1 || dgrp) {
+      if (kind == 2) {
+        // designated finaliser of a multi-tile group: own segment sums from
+        // shared memory, then the other tiles' part slots once they are in
+        for (int col = tid; col < CH; col += blockDim.x)
+          for (int i = 0; i < s1 - s0; ++i) pr[s_row[i] - r0][col] -= sp[i][col];
+        if (tid == 0) {
+          const int32_t* cnt = t.counters + (int64_t)gi * n_chunks + chunk;
+          while (ld_relaxed(cnt) != nt - 1) __nanosleep(32);
+        }
+        __syncthreads();
+        fence_acq_rel();
+        TRIW_TR(3);
+        sub_slots();
+      } else if (nt > 1 || dgrp) {
         // 2a: per (tile, row) sums in segment order -> part slots; count in;
-        // the last tile of a sparse group finalises it (a dense-region
-        // group is finalised by its dense task)
+        // a sparse group is finalised by its designated last tile (kind 2),
+        // a dense-region group by its dense task (kind 1)
         for (int col = tid; col < CH; col += blockDim.x) {
           double a = 0.0;
           for (int i = 0; i < s1 - s0; ++i) {
@@ -327,23 +376,11 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         }
         __threadfence();
         __syncthreads();
-        if (tid == 0) last_s = atomicAdd(t.counters + (int64_t)gi * n_chunks + chunk, 1) == nt - 1 && !dgrp;
-        __syncthreads();
+        if (tid == 0) atomicAdd(t.counters + (int64_t)gi * n_chunks + chunk, 1);
         TRIW_TR(3);
-        if (!last_s) continue;
-        __threadfence();
-        // 2b: P = B - sum of the row's slots (tile order)
-        p_from_slots([](int, int) { return 0.0; });
+        continue;
       } else {
-        // 2: one-tile group: P = B - segment sums of each row (segment order)
-        for (int i = tid; i < g * CH; i += blockDim.x) {
-          const int r = i / CH, col = i - r * CH;
-          const int p = r0 + r;
-          pr[r][col] = col >= w ? 0.0
-                                : FWD ? *wseg_ptr(io, __ldg(t.io_row + p), c0 + col)
-                                      : __ldcg(work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + col);
-        }
-        __syncthreads();
+        // 2: one-tile group: P = B (prefetched) - segment sums of each row
         for (int col = tid; col < CH; col += blockDim.x)
           for (int i = 0; i < s1 - s0; ++i) pr[s_row[i] - r0][col] -= sp[i][col];
       }

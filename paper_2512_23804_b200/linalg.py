@@ -307,10 +307,14 @@ def wide_tiles(strict: csr_matrix, gptr: np.ndarray, order: np.ndarray, dense: t
         if is_dense and not tiles[-1]:
             tiles = []  # no entries left of the region: the dense task alone
         group_ntiles[g] = len(tiles)
-        for tl in tiles:
+        for ti, tl in enumerate(tiles):
+            # the last tile of a multi-tile sparse group is its designated
+            # finaliser (kind 2): it keeps its own sums in shared memory and
+            # only the other tiles get part slots
+            designated = len(tiles) > 1 and not is_dense and ti == len(tiles) - 1
             prev = -1
             for (p, e0, e1) in tl:
-                if len(tiles) > 1 or is_dense:
+                if (len(tiles) > 1 or is_dense) and not designated:
                     if p != prev:
                         row_slots[p].append(n_slots)
                         n_slots += 1
@@ -323,7 +327,7 @@ def wide_tiles(strict: csr_matrix, gptr: np.ndarray, order: np.ndarray, dense: t
                 seg_e1.append(e1)
             tile_group.append(int(g))
             tile_seg.append(len(seg_row))
-            tile_kind.append(0)
+            tile_kind.append(2 if designated else 0)
         if is_dense:
             tile_group.append(int(g))
             tile_seg.append(len(seg_row))

@@ -356,14 +356,53 @@ class SteadyKKT:
             self._cache["kkt_prog"] = prog
         return prog
 
+    def kkt_programs_split(self) -> tuple[DeviceProgram, DeviceProgram]:
+        """The KKT matvec as two launches: the stiffness-coupled inputs (Y, L:
+        2 x ceil(n_xi/128) column groups <= 8 -> the warp-specialised 9-point
+        kernel) writing all three outputs, then the mass-only input U
+        accumulated into r_u and r_l (init = the outputs)."""
+        progs = self._cache.get("kkt_split")
+        if progs is None:
+            n_xi, T, m = self.n_xi, self.n_terms, self.mass_slice
+            full = (0, n_xi)
+            wdiag = self.triple.objective_weight.tocsr()
+            eye = sp.identity(n_xi, format="csr")
+            cps: list[Coupling | None] = []
+            # inputs: 0=Y, 1=L ; outputs: 0=r_y, 1=r_u, 2=r_l
+            cps.append(coupling_from_csr(0, 0, m, wdiag, full, full, 1.0))  # (M Y) diag(h^gamma)
+            for t in range(T):
+                h = self.triple.matrices[t].tocsr()
+                cps.append(coupling_from_csr(1, 0, t, h, full, full, -1.0))  # - A^T L
+                cps.append(coupling_from_csr(0, 2, t, h, full, full, -1.0))  # - A Y
+            cps.append(coupling_from_csr(1, 1, m, eye, full, full, 1.0))  # M L
+            p_yl = DeviceProgram(cps, (n_xi, n_xi, n_xi), n_inputs=2)
+            cps_u = [coupling_from_csr(0, 0, m, eye, full, full, self.beta),  # r_u += beta M U
+                     coupling_from_csr(0, 1, m, eye, full, full, 1.0)]  # r_l += M U
+            p_u = DeviceProgram(cps_u, (n_xi, n_xi), n_inputs=1)
+            progs = (p_yl, p_u)
+            self._cache["kkt_split"] = progs
+        return progs
+
     def algorithmic_bytes(self) -> int:
         """KKT matvec floor: 3 blocks read + 3 written + (T+1) value slices."""
         nnz_h = sum(int(h.nnz) for h in self.triple.matrices[: self.n_terms])
         return 48 * self.n_h * self.n_xi + self.pattern.algorithmic_bytes + 12 * (nnz_h + 2 * self.n_xi)
 
 
+# SGKKT_KKT_SPLIT=0: the KKT matvec as one 3-input launch (12 column groups at
+# config 5 -> the alternating 16-warp kernel) instead of two launches
+KKT_SPLIT = __import__("os").environ.get("SGKKT_KKT_SPLIT", "1") != "0"
+
+
 def steady_kkt_apply_device(sys: SteadyKKT, y: torch.Tensor, u: torch.Tensor, lam: torch.Tensor,
                             out: tuple[torch.Tensor, torch.Tensor, torch.Tensor]) -> None:
+    if KKT_SPLIT and sys.n_xi > 128:
+        p_yl, p_u = sys.kkt_programs_split()
+        run_program(sys.pattern, p_yl, [(y, 0), (lam, 0)], [(out[0], 0), (out[1], 0), (out[2], 0)],
+                    alpha=[1.0] * 3, beta=[0.0] * 3)
+        run_program(sys.pattern, p_u, [(u, 0)], [(out[1], 0), (out[2], 0)], [(out[1], 0), (out[2], 0)],
+                    alpha=[1.0] * 2, beta=[1.0] * 2)
+        return
     run_program(sys.pattern, sys.kkt_program(), [(y, 0), (u, 0), (lam, 0)],
                 [(out[0], 0), (out[1], 0), (out[2], 0)], alpha=[1.0] * 3, beta=[0.0] * 3)
 

@@ -67,7 +67,16 @@ def _emulate(strict, gptr, order, dinv, w, b, dense=(0, 0)):
             sp_.append(strict.data[e0:e1] @ x[cols])
         nt = int(w["group_ntiles"][g])
         is_dense = d1 > d0 and d0 <= a < d1
-        if nt > 1 or is_dense:
+        if w["tile_kind"][t] == 2:
+            # designated finaliser: the group's other tiles are done
+            assert done_tiles.get(g, 0) == nt - 1
+            p_rows = b[a:bb].copy()
+            for s in range(ts[t], ts[t + 1]):
+                p_rows[w["seg_row"][s] - a] -= sp_[s - ts[t]]
+            for r in range(a, bb):
+                for q in range(w["row_slot_ptr"][r], w["row_slot_ptr"][r + 1]):
+                    p_rows[r - a] -= part[w["row_slot"][q]]
+        elif nt > 1 or is_dense:
             acc = None
             for s in range(ts[t], ts[t + 1]):
                 v = sp_[s - ts[t]]
