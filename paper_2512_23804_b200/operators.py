@@ -389,9 +389,12 @@ class SteadyKKT:
         return 48 * self.n_h * self.n_xi + self.pattern.algorithmic_bytes + 12 * (nnz_h + 2 * self.n_xi)
 
 
-# SGKKT_KKT_SPLIT=0: the KKT matvec as one 3-input launch (12 column groups at
-# config 5 -> the alternating 16-warp kernel) instead of two launches
-KKT_SPLIT = __import__("os").environ.get("SGKKT_KKT_SPLIT", "1") != "0"
+# SGKKT_KKT_SPLIT=1: the KKT matvec as two launches (Y/L couplings on the
+# warp-specialised kernel + a mass-only launch for U) instead of one 3-input
+# launch (12 column groups at config 5 -> the alternating 16-warp kernel).
+# Measured at config 5: 0.594 ms split vs 0.446 ms fused (tools/time_kkt.py),
+# so the fused launch stays the default.
+KKT_SPLIT = __import__("os").environ.get("SGKKT_KKT_SPLIT", "0") == "1"
 
 
 def steady_kkt_apply_device(sys: SteadyKKT, y: torch.Tensor, u: torch.Tensor, lam: torch.Tensor,
