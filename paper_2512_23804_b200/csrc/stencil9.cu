@@ -732,7 +732,24 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
     // the right one.  Sliding from p-1 is one call (dxn = 1); a line start or
     // the range start is three calls (dxn = -1, 0, 1) through the SAME code
     // (a second load path made ptxas spill the window at 128 registers).
+    // L2 prefetch of the window column node p will need SGK_GRID_PF rows
+    // later (lines y-1..y+1 at x + 1 + SGK_GRID_PF): lane l < 24 fetches one
+    // 128-byte line of the warp's 1 KB slice of one node, so the next rows'
+    // first-touch V loads hit L2 instead of waiting on HBM
+#ifndef SGK_GRID_PF
+#define SGK_GRID_PF 2
+#endif
+    auto prefetch_col = [&](int p) {
+      if (SGK_GRID_PF <= 0) return;
+      const int iy = p / nx, ix = p - iy * nx + 1 + SGK_GRID_PF;
+      const int dy = lane / 8 - 1, ln = lane & 7;
+      if (lane < 24 && ix < nx && iy + dy >= 0 && iy + dy < ny) {
+        const double* a = rvb + (int64_t)(p + dy * nx + 1 + SGK_GRID_PF) * rld + 16 * ln;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    };
     auto window = [&](int p, bool restart) {
+      prefetch_col(p);
       const int iy = p / nx, ix = p - iy * nx;
       const bool yl = iy > 0, yh = iy + 1 < ny;
 #pragma unroll 1

@@ -190,6 +190,18 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         pr[r][col] -= sum;
       }
     };
+    // pr[row] -= the tile's segment sums of that row, one thread per (run of
+    // one row's consecutive segments, column), segment order within a run
+    auto sub_runs = [&]() {
+      const int ns = s1 - s0;
+      for (int it = tid; it < ns * CH; it += blockDim.x) {
+        const int i0 = it / CH, col = it - i0 * CH;
+        if (i0 > 0 && s_row[i0 - 1] == s_row[i0]) continue;  // not a run start
+        double a = sp[i0][col];
+        for (int i = i0 + 1; i < ns && s_row[i] == s_row[i0]; ++i) a += sp[i][col];
+        pr[s_row[i0] - r0][col] -= a;
+      }
+    };
     // P rows = B (the right-hand side rows of the group; static)
     auto init_b = [&]() {
       for (int i = tid; i < g * CH; i += blockDim.x) {
@@ -301,6 +313,19 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         s_e1[i] = __ldg(t.seg_e1 + s0 + i);
         s_slot[i] = __ldg(t.seg_slot + s0 + i);
       }
+      // the first segment's entries are static: every warp fetches its
+      // (column, value) batch before the dependency wait
+      int pcj = 0;
+      double pvj = 0.0;
+      {
+        const int sf = s0 + warp;
+        if (sf < s1) {
+          const int e0 = __ldg(t.seg_e0 + sf), e1 = __ldg(t.seg_e1 + sf);
+          const int e = e0 + lane;
+          pcj = __ldg(t.colind + (e < e1 ? e : e0));
+          pvj = e < e1 ? __ldg(t.vals + e) : 0.0;
+        }
+      }
       // 0: wait for the groups this tile's entries read (warp 0 polls, one fence)
       if (warp == 0) {
         const int da = __ldg(t.tile_dep_ptr + tile), db = __ldg(t.tile_dep_ptr + tile + 1);
@@ -322,8 +347,9 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         // padding entries re-read the segment's first entry (a finished
         // dependency: final, finite) with weight 0
         const int e = e0 + lane;
-        const int cj = __ldg(t.colind + (e < e1 ? e : e0));
-        const double vj = e < e1 ? __ldg(t.vals + e) : 0.0;
+        const bool first = s == s0 + warp;
+        const int cj = first ? pcj : __ldg(t.colind + (e < e1 ? e : e0));
+        const double vj = first ? pvj : (e < e1 ? __ldg(t.vals + e) : 0.0);
         const int cnt = e1 - e0;
         for (int jb = 0; jb < cnt; jb += WB) {
           double xv[WB][CPL];
@@ -349,8 +375,7 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
       if (kind == 2) {
         // designated finaliser of a multi-tile group: own segment sums from
         // shared memory, then the other tiles' part slots once they are in
-        for (int col = tid; col < CH; col += blockDim.x)
-          for (int i = 0; i < s1 - s0; ++i) pr[s_row[i] - r0][col] -= sp[i][col];
+        sub_runs();
         if (tid == 0) {
           const int32_t* cnt = t.counters + (int64_t)gi * n_chunks + chunk;
           while (ld_relaxed(cnt) != nt - 1) __nanosleep(32);
@@ -363,16 +388,16 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         // 2a: per (tile, row) sums in segment order -> part slots; count in;
         // a sparse group is finalised by its designated last tile (kind 2),
         // a dense-region group by its dense task (kind 1)
-        for (int col = tid; col < CH; col += blockDim.x) {
-          double a = 0.0;
-          for (int i = 0; i < s1 - s0; ++i) {
-            a += sp[i][col];
-            const int slot = s_slot[i];
-            if (i + 1 == s1 - s0 || s_slot[i + 1] != slot) {
-              __stcg(part + (int64_t)slot * ldw + c0 + col, a);
-              a = 0.0;
-            }
-          }
+        // one thread per (run of one row's consecutive segments, column):
+        // the run's segment sums in order -> its slot
+        const int ns = s1 - s0;
+        for (int it = tid; it < ns * CH; it += blockDim.x) {
+          const int i0 = it / CH, col = it - i0 * CH;
+          if (i0 > 0 && s_slot[i0 - 1] == s_slot[i0]) continue;  // not a run start
+          double a = sp[i0][col];
+          int i = i0 + 1;
+          for (; i < ns && s_slot[i] == s_slot[i0]; ++i) a += sp[i][col];
+          __stcg(part + (int64_t)s_slot[i0] * ldw + c0 + col, a);
         }
         __threadfence();
         __syncthreads();
@@ -381,8 +406,7 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         continue;
       } else {
         // 2: one-tile group: P = B (prefetched) - segment sums of each row
-        for (int col = tid; col < CH; col += blockDim.x)
-          for (int i = 0; i < s1 - s0; ++i) pr[s_row[i] - r0][col] -= sp[i][col];
+        sub_runs();
       }
     }
     if (!minv_early) load_minv();
