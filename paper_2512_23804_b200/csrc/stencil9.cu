@@ -418,6 +418,14 @@ __host__ __device__ inline Smem9 smem9_ws_layout(int n_slices, const sgk_program
   return s;
 }
 
+// speed-of-light probes (debug builds only, results wrong): SGK_DBG_QEND
+// truncates the producers' step loop, SGK_DBG_NPAIR the consumers' gather
+#ifndef SGK_DBG_QEND
+#define SGK_DBG_QEND rq1
+#endif
+#ifndef SGK_DBG_NPAIR
+#define SGK_DBG_NPAIR (ccnt[chunk] >> 1)
+#endif
 template <int MAXOUT, bool ONEOUT>
 __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
                                                             ViewSet out, ViewSet init, ScalarSet alpha,
@@ -526,7 +534,7 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
           p01 = a2[0];
           p23 = a2[1];
         }
-        for (int q = rq0; q < rq1; ++q, ubq += kGroupCols) {
+        for (int q = rq0; q < SGK_DBG_QEND; ++q, ubq += kGroupCols) {
           const int rec = recn;
           double* ub = ubq + (lane ^ (rec >> 16));
           double a[10];
@@ -579,7 +587,7 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
       for (int rb = 0; rb < MAXOUT; ++rb) {
         const int chunk = cw + rb * 8;
         if (chunk >= n_chunks) break;
-        const int npair = ccnt[chunk] >> 1;
+        const int npair = SGK_DBG_NPAIR;
         const uint2* gp = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
         double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll 2
@@ -630,12 +638,25 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
 // position order (dy+1)*3 + (dx+1) with zeros for missing neighbours; a
 // missing neighbour's V load is redirected to the row's own node (finite
 // value times a zero coefficient).  Gather and barriers as stencil9_ws_kernel.
+// V staging of the grid kernel: per producer warp 3 nodes x 4 slots x 32
+// lanes doubles (the next row's new window column, cp.async'ed one row ahead)
+constexpr int kVStage = 8 * 3 * kCols * 32;
+__host__ __device__ inline Smem9 smem9_grid_layout(int n_slices, const sgk_program9& p) {
+  Smem9 s = smem9_ws_layout(n_slices, p);
+  s.total = align16(s.total) + sizeof(double) * kVStage;
+  return s;
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
 template <int MAXOUT, bool ONEOUT>
 __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk_program9 prog, ViewSet in,
                                                               ViewSet out, ViewSet init, ScalarSet alpha,
                                                               ScalarSet beta) {
   extern __shared__ __align__(16) unsigned char sm[];
-  const Smem9 L = smem9_ws_layout(gp.n_slices, prog);
+  const Smem9 L = smem9_grid_layout(gp.n_slices, prog);
   double* coef_s = reinterpret_cast<double*>(sm + L.coef);
   double* ubuf = reinterpret_cast<double*>(sm + L.ubuf);
   double* ctab = reinterpret_cast<double*>(sm + L.ctab);
@@ -768,12 +789,65 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
         }
       }
     };
+    // the new window column of (non-restart) node p, cp.async'ed into this
+    // warp's staging slots: lane L copies exactly the 12 doubles it will
+    // read back (node k, slot c at [(k*kCols + c)*32 + L]), so no warp sync
+    // (recomputed at each use: keeping it live across the product loop
+    // costs the registers the window needs)
+#define SGK_VST (reinterpret_cast<double*>(sm + L.total) - kVStage + (tid >> 5) * (3 * kCols * 32) + (tid & 31))
+    auto stage_v = [&](int p, int dxn) {
+      double* vst = SGK_VST;
+      const int iy = p / nx, ix = p - iy * nx;
+      const bool yl = iy > 0, yh = iy + 1 < ny, xok = ix + dxn >= 0 && ix + dxn < nx;
+#pragma unroll
+      for (int dy = -1; dy <= 1; ++dy) {
+        const bool ok = (dy < 0 ? yl : (dy > 0 ? yh : true)) && xok;
+        const double* b = nbase(p, ok, dy * nx + dxn);
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) cp_async8(vst + ((dy + 1) * kCols + c) * 32, b + 32 * c);
+      }
+    };
+    // shift reads the last loaded column: it also retires that column's LDS
+    // before the staging slots are overwritten
+    auto window_shift = [&]() {
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) {
+          rv[c][k * 3 + 0] = rv[c][k * 3 + 1];
+          rv[c][k * 3 + 1] = rv[c][k * 3 + 2];
+        }
+    };
+    auto window_load = [&]() {
+      const double* vst = SGK_VST;
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) rv[c][k * 3 + 2] = vst[(k * kCols + c) * 32];
+    };
+    // the ONE code path that writes the window registers (two paths made
+    // ptxas spill at 128 registers): a slide consumes the column staged a
+    // product phase earlier; a restart stages and consumes its three columns
+    // synchronously (once per grid-line segment)
+    auto window_unified = [&](int p, bool restart) {
+#pragma unroll 1
+      for (int k = restart ? 0 : 2; k < 3; ++k) {
+        window_shift();
+        if (restart) {
+          stage_v(p, k - 1);
+          cp_async_commit();
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        window_load();
+      }
+    };
+    (void)window;
     int sg = s_first + blockIdx.x, node = 0, nend = 0;
     bool have = sg <= s_last;
     if (have) seg_range(sg, node, nend);
     if (have) stage(node - A, 0);
     cp_async_commit();
-    if (active && have) window(node, true);
+    if (active && have) window_unified(node, true);
     int it = 0;
     for (; have; ++it) {
       const int cb = it & 1;
@@ -783,6 +857,9 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       bar_sync_n(5, 256);  // this row's coefficients visible; every producer is done with row it-1
       if (have_n) stage(node_n - A, cb ^ 1);
+      // the barrier has retired the last staged column's LDS: stage the next
+      // row's column now, a whole product phase ahead of its use
+      if (active && have_n && !restart_n) stage_v(node_n, 1);
       cp_async_commit();
       if (it >= 2) bar_sync_n(3 + cb, 512);  // consumers are done with U buffer cb (row it-2)
       if (active) {
@@ -795,7 +872,7 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
           p01 = a2[0];
           p23 = a2[1];
         }
-        for (int q = rq0; q < rq1; ++q, ubq += kGroupCols) {
+        for (int q = rq0; q < SGK_DBG_QEND; ++q, ubq += kGroupCols) {
           const int rec = recn;
           double* ub = ubq + (lane ^ (rec >> 16));
           double a[10];
@@ -820,7 +897,7 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
         }
       }
       bar_arrive_n(1 + cb, 512);  // U buffer cb holds row it
-      if (active && have_n) window(node_n, restart_n);  // next row's window: overlaps the next waits
+      if (active && have_n) window_unified(node_n, restart_n);  // next row's window
       sg = sg_n;
       node = node_n;
       nend = nend_n;
@@ -854,7 +931,7 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
       for (int rb = 0; rb < MAXOUT; ++rb) {
         const int chunk = cw + rb * 8;
         if (chunk >= n_chunks) break;
-        const int npair = ccnt[chunk] >> 1;
+        const int npair = SGK_DBG_NPAIR;
         const uint2* gpe = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
         double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll 2
@@ -898,7 +975,7 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
 template <int MAXOUT, bool ONEOUT>
 static int launch9grid(const sgk_grid9& gp, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
                        const ViewSet& init, const ScalarSet& a, const ScalarSet& b, cudaStream_t st) {
-  const Smem9 L = smem9_ws_layout(gp.n_slices, prog);
+  const Smem9 L = smem9_grid_layout(gp.n_slices, prog);
   static bool attr_set = false;
   if (!attr_set) {
     int dev = 0, optin = 0;
