@@ -247,10 +247,23 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
             }
             d_pref = j;
           }
-          __nanosleep(32);
+          // the critical chain of the solve runs through these blocks: the
+          // task awaiting the block right before its own spins on that flag;
+          // tasks further down the chain back off (fewer L2 polls from the
+          // CTAs that cannot make progress anyway)
+          if (warp == 0) {
+            if (bi - j > 2) {
+              __nanosleep(1000);
+            } else {
+              const int32_t* fl = t.flags + (int64_t)(t.dense_g0 + j) * n_chunks + chunk;
+              for (int spin = 0; spin < 256 && ld_relaxed(fl) != epoch; ++spin) {
+              }
+            }
+          }
           continue;
         }
         fence_acq_rel();
+        if (j + ready == bi) TRIW_TR(1);  // dense task: the awaited last block detected
         for (int jj = j; jj < j + ready; ++jj) {
           for (int i = tid; i < WG * CH; i += blockDim.x) {
             const int k = i / CH, c = i - k * CH;
@@ -432,9 +445,22 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         if (!FWD && col < w) *wseg_ptr(io, __ldg(t.io_row + p), c0 + col) = acc[k];
       }
     }
+#ifndef SGK_TRIW_ONE_FENCE
+#define SGK_TRIW_ONE_FENCE 1
+#endif
+#if SGK_TRIW_ONE_FENCE
+    // release: the barrier orders every thread's stores before thread 0's
+    // gpu-scope fence (cumulativity), so one fence publishes the group
+    __syncthreads();
+    if (tid == 0) {
+      fence_acq_rel();
+      st_relaxed(t.flags + (int64_t)gi * n_chunks + chunk, epoch);
+    }
+#else
     fence_acq_rel();
     __syncthreads();
     if (tid == 0) st_relaxed(t.flags + (int64_t)gi * n_chunks + chunk, epoch);
+#endif
     TRIW_TR(4);
     TRIW_TR(5);
   }

@@ -61,3 +61,17 @@ for fwd, tw, bufs in ((1, fac.wl, fac.wl_bufs), (0, fac.wu, fac.wu_bufs)):
         sel = (ent >= lo) & (ent < hi)
         if sel.any():
             print(f"   tiles with {lo}-{hi} entries: {sel.sum()}, segments phase median {np.median(tr[sel, 2] - tr[sel, 1]):.2f} us")
+
+    # dense-region chain: per block, publish(i-1) -> detect(i) -> applied -> publish(i)
+    kind = bufs[12].cpu().numpy()
+    dk = np.nonzero(kind[tile] == 1)[0]
+    if len(dk):
+        c0 = dk[(np.arange(nt)[dk] % nch) == 0]  # chunk 0 of each dense task
+        pub = tr[c0, 4]
+        det = tr[c0, 1]
+        app = tr[c0, 2]
+        if len(c0) > 2:
+            prop = det[1:] - pub[:-1]
+            print(f"   dense chain ({len(c0)} blocks, chunk 0): median us: publish(i-1)->detect(i) {np.median(prop):.2f}"
+                  f"  detect->applied {np.median(app[1:] - det[1:]):.2f}  applied->publish {np.median(pub[1:] - app[1:]):.2f}"
+                  f"  block period {np.median(np.diff(pub)):.2f}")
