@@ -14,10 +14,14 @@ $(LIB): $(SRC) paper_2512_23804_b200/csrc/sgk_common.cuh include/sgkkt_b200.h
 trace: $(SRC)
 	mkdir -p build_variants && $(NVCC) $(ARCH) $(NVFLAGS) -DSGK_TRIW_TRACE -shared -o build_variants/libsgkkt_triwtrace.so $(SRC)
 
+# phase-trace build of the warp-specialised matvec kernel (tools/s9_trace.py)
+s9trace: $(SRC)
+	mkdir -p build_variants && $(NVCC) $(ARCH) $(NVFLAGS) -DSGK_S9_TRACE -shared -o build_variants/libsgkkt_s9trace.so $(SRC)
+
 ptxas:
 	$(NVCC) $(ARCH) $(NVFLAGS) -Xptxas -v -c -o /tmp/sgk_probe.o paper_2512_23804_b200/csrc/galerkin.cu
 
 clean:
 	rm -f $(LIB)
 
-.PHONY: all clean ptxas
+.PHONY: all clean ptxas trace s9trace

@@ -16,6 +16,7 @@
 //     so per row only the U values move through shared memory.
 // Rows are processed grid-stride by persistent CTAs; the row's coefficient
 // block (n_slices x 10 doubles) is staged with 16-byte loads.
+#include <cstdio>
 #include <cstdlib>
 
 #include "sgk_common.cuh"
@@ -420,11 +421,25 @@ __host__ __device__ inline Smem9 smem9_ws_layout(int n_slices, const sgk_program
 
 // speed-of-light probes (debug builds only, results wrong): SGK_DBG_QEND
 // truncates the producers' step loop, SGK_DBG_NPAIR the consumers' gather
+#ifndef SGK_GATHER_UNROLL
+#define SGK_GATHER_UNROLL 2
+#endif
+constexpr int kGatherUnroll = SGK_GATHER_UNROLL;
 #ifndef SGK_DBG_QEND
 #define SGK_DBG_QEND rq1
 #endif
 #ifndef SGK_DBG_NPAIR
 #define SGK_DBG_NPAIR (ccnt[chunk] >> 1)
+#endif
+// trace build (-DSGK_S9_TRACE, tools/s9_trace.py): CTA 0 stamps clock64() at
+// the phase boundaries of its first 256 rows (producer warps 0 and 7,
+// consumer warp 8); the producers additionally wait for the V registers
+// before the products so the exposed load latency shows up as its own phase
+#ifdef SGK_S9_TRACE
+__device__ long long sgk_s9_trace[3][256][8];
+#define S9_STAMP(w, k) do { if (blockIdx.x == 0 && lane == 0 && it < 256) sgk_s9_trace[w][it][k] = clock64(); } while (0)
+#else
+#define S9_STAMP(w, k) do {} while (0)
 #endif
 template <int MAXOUT, bool ONEOUT>
 __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
@@ -519,11 +534,23 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
     for (; row < r_end; row += r_step, ++it) {
       const int cb = it & 1;
       const int next = row + r_step;
+      const int tw = warp == 0 ? 0 : 1;
+      (void)tw;
+      if (warp == 0 || warp == 7) S9_STAMP(tw, 0);
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       bar_sync_n(5, 256);  // this row's coefficients visible; every producer is done with row it-1
+      if (warp == 0 || warp == 7) S9_STAMP(tw, 1);
       if (next < r_end) stage(next, cb ^ 1);
       cp_async_commit();
       if (it >= 2) bar_sync_n(3 + cb, 512);  // consumers are done with U buffer cb (row it-2)
+      if (warp == 0 || warp == 7) S9_STAMP(tw, 2);
+#ifdef SGK_S9_TRACE
+      if (active) {  // consume the last-issued V loads: the scoreboard wait lands here
+        const double chk = rv[kCols - 1][8] + rv[0][8] + rv[kCols - 1][0];
+        if (chk == 1.2345e-300) ubuf[prog.n_ubuf] = chk;
+      }
+      if (warp == 0 || warp == 7) S9_STAMP(tw, 3);
+#endif
       if (active) {
         const double* crow = coef_s + cb * ncoef;
         double* ubq = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ubuf) + cb * ustride) + rbase;
@@ -558,8 +585,10 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
           for (int c = 0; c < kCols; ++c) ub[32 * c] = dot9(a, rv[c]);
         }
       }
+      if (warp == 0 || warp == 7) S9_STAMP(tw, 4);
       bar_arrive_n(1 + cb, 512);  // U buffer cb holds row it
       if (active && next < r_end) load_v(next);  // prefetch: overlaps the next waits
+      if (warp == 0 || warp == 7) S9_STAMP(tw, 5);
     }
     // match the consumers' last EMPTY arrivals
     for (int k = (it >= 2 ? it - 2 : 0); k < it; ++k) bar_sync_n(3 + (k & 1), 512);
@@ -575,7 +604,9 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
     int it = 0;
     for (int row = r_begin; row < r_end; row += r_step, ++it) {
       const int cb = it & 1;
+      if (cw == 0) S9_STAMP(2, 0);
       bar_sync_n(1 + cb, 512);  // products of this row are in U buffer cb
+      if (cw == 0) S9_STAMP(2, 1);
       const unsigned char* smb = sm + cb * ustride;  // U addresses of buffer cb
       double* orow = nullptr;
       const double* irow = nullptr;
@@ -590,7 +621,7 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
         const int npair = SGK_DBG_NPAIR;
         const uint2* gp = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
         double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll 2
+#pragma unroll kGatherUnroll
         for (int e = 0; e < npair; ++e, gp += 32) {
           const uint2 w = *gp;
           acc0 = fma(*reinterpret_cast<const double*>(sm + (w.x & 0x3FFF)),
@@ -621,6 +652,7 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
           }
         }
       }
+      if (cw == 0) S9_STAMP(2, 2);
       bar_arrive_n(3 + cb, 512);  // done reading U buffer cb
     }
   }
@@ -1202,6 +1234,12 @@ __global__ void grid9_coef_kernel(int32_t n_rows, int32_t n_slices, int32_t nx, 
   for (int k = 0; k < 10; ++k) coefg[i * 10 + k] = acc[k];
 }
 }  // namespace sgk
+
+#ifdef SGK_S9_TRACE
+extern "C" int sgk_s9_trace_read(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, sgk::sgk_s9_trace, sizeof(long long) * 3 * 256 * 8);
+}
+#endif
 
 extern "C" int sgk_grid9_coef(int32_t n_rows, int32_t n_slices, int32_t nx, const int32_t* colind9,
                               const double* coef10, double* coefg, void* stream) {
