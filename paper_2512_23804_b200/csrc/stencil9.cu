@@ -659,6 +659,309 @@ __global__ void __launch_bounds__(512, 1) stencil9_ws_kernel(sgk_pattern9 pat, s
 }
 
 // ---------------------------------------------------------------------------
+// TMA / mbarrier pipeline of the warp-specialised kernel (sm_100a).  Same
+// roles, tables and arithmetic as stencil9_ws_kernel (bit-identical results);
+// what changes is the hand-over:
+//   * a row's coefficient block and its 9 column indices arrive by two bulk
+//     copies (cp.async.bulk, complete_tx on an mbarrier) into a 4-slot ring,
+//     issued four rows ahead by one consumer thread — the producers no
+//     longer stage coefficients themselves, so the producer-wide barrier and
+//     the dependent global colind load in front of the V loads are gone;
+//   * FULL/EMPTY are mbarriers (one arrival per warp): a producer warp waits
+//     only for the consumers, never for the other producer warps, so the
+//     warps' non-product phases (V latency, waits) overlap other warps'
+//     products instead of lining up behind a named barrier;
+//   * NPW = 12 (programs with 9..12 column groups, e.g. the 3-input KKT
+//     matvec): 12 producer + 8 consumer warps; the 640-thread CTA starts at 96
+//     registers per thread and setmaxnreg moves the producers to 128 and the
+//     consumers to 48 (the CTA's register total is unchanged).
+// Measured and dropped (config 4, gpurun_out/g40..g43): V registers of two
+// rows (setmaxnreg 200/56; 1.088 ms), two steps = 8 DFMA chains per producer
+// iteration with coefficients a pair ahead (1.145 ms), coefficient selection
+// from registers in the gather (1.130 ms) against 1.070 ms for this form.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+
+constexpr int kRing = 4;  // coefficient ring depth (rows in flight)
+// ring slot: the row's n_slices x 10 coefficients, then a 64-byte window of
+// colind9 that starts at the 16-byte boundary below the row's 9 indices
+__host__ __device__ inline size_t tma_slot_bytes(int n_slices) { return align16(sizeof(double) * 10 * (size_t)n_slices) + 64; }
+__host__ __device__ inline size_t smem9_tma_total(int n_slices, const sgk_program9& p) {
+  return smem9_ws_layout(n_slices, p).total + kRing * tma_slot_bytes(n_slices);
+}
+
+template <int MAXOUT, bool ONEOUT, int NPW>
+__global__ void __launch_bounds__((NPW + 8) * 32, 1) stencil9_tma_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
+                                                             ViewSet out, ViewSet init, ScalarSet alpha,
+                                                             ScalarSet beta) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const Smem9 L = smem9_ws_layout(pat.n_slices, prog);
+  double* ubuf = reinterpret_cast<double*>(sm + L.ubuf);
+  double* ctab = reinterpret_cast<double*>(sm + L.ctab);
+  int32_t* steps = reinterpret_cast<int32_t*>(sm + L.steps);
+  int32_t* groups = reinterpret_cast<int32_t*>(sm + L.groups);
+  int32_t* ccnt = reinterpret_cast<int32_t*>(sm + L.ccnt);
+  int32_t* coff = reinterpret_cast<int32_t*>(sm + L.coff);
+  uint32_t* gent = reinterpret_cast<uint32_t*>(sm + L.gent);
+  unsigned char* ring = sm + L.total;
+  const int ustride = (int)(align16(sizeof(double) * ((size_t)prog.n_ubuf + 64)));  // bytes between U buffers
+  const int ncoef = pat.n_slices * 10;
+  const int coef_bytes = ncoef * (int)sizeof(double);
+  const int slot_bytes = (int)tma_slot_bytes(pat.n_slices);
+  constexpr bool REGS = NPW > 8;  // 640 threads start at 96 registers: producers 128, consumers 48 (12*128 + 8*48 = 20*96)
+  constexpr int kIssuer = NPW * 32;  // first consumer thread: issues the bulk copies
+  __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2], bar_coef[kRing];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const bool producer = warp < NPW;
+  const int n_chunks = prog.n_chunks;
+  __shared__ const double* in_ptr[SGK_MAX_IO];
+  __shared__ int64_t in_ld[SGK_MAX_IO];
+  if (tid < SGK_MAX_IO) {
+    const sgk_view& vv = pick(in, tid);
+    in_ptr[tid] = vv.ptr + vv.col0;
+    in_ld[tid] = vv.ld;
+  }
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_full[b], NPW);
+      mbar_init(&bar_empty[b], 8);
+    }
+    for (int b = 0; b < kRing; ++b) mbar_init(&bar_coef[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < prog.n_coef; i += blockDim.x) ctab[i] = prog.coef_tab[i];
+  for (int i = tid; i < prog.n_steps; i += blockDim.x) steps[i] = prog.step_rec[i];
+  for (int i = tid; i < 4 * (prog.n_groups + 1); i += blockDim.x) groups[i] = prog.group_info[i];
+  for (int i = tid; i < n_chunks; i += blockDim.x) {
+    ccnt[i] = prog.gather_ptr[2 * i];
+    coff[i] = prog.gather_ptr[2 * i + 1];
+  }
+  for (int i = tid; i < prog.n_gather; i += blockDim.x) gent[i] = prog.gather_ent[i];
+  for (int i = tid; i < 64; i += blockDim.x) {
+    ubuf[prog.n_ubuf + i] = 0.0;
+    reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ubuf) + ustride)[prog.n_ubuf + i] = 0.0;
+  }
+  __syncthreads();
+
+  const int r_begin = blockIdx.x, r_step = gridDim.x;
+  const int n_it = r_begin < pat.n_rows ? (pat.n_rows - r_begin + r_step - 1) / r_step : 0;
+  // one thread: the two bulk copies of iteration itx's row into ring slot itx % kRing
+  auto issue_row = [&](int itx) {
+    const int64_t row = r_begin + (int64_t)itx * r_step;
+    uint64_t* bar = &bar_coef[itx & (kRing - 1)];
+    unsigned char* dst = ring + (itx & (kRing - 1)) * slot_bytes;
+    // 16-byte window around the row's 9 indices (a row-range launch shifts colind9 by 36-byte rows)
+    const uintptr_t ci = reinterpret_cast<uintptr_t>(pat.colind9) + (uintptr_t)row * 36;
+    const uintptr_t ci0 = ci & ~uintptr_t(15);
+    const uintptr_t ci_end = (reinterpret_cast<uintptr_t>(pat.colind9) + (uintptr_t)pat.n_rows * 36 + 15) &
+                             ~uintptr_t(15);  // allocation granularity covers the round-up
+    const uint32_t ci_bytes = (uint32_t)(ci_end - ci0 < 64 ? ci_end - ci0 : 64);
+    mbar_expect_tx(bar, (uint32_t)coef_bytes + ci_bytes);
+    bulk_load(dst, pat.coef10 + row * ncoef, (uint32_t)coef_bytes, bar);
+    bulk_load(dst + slot_bytes - 64, reinterpret_cast<const void*>(ci0), ci_bytes, bar);
+  };
+  if (producer) {
+    if constexpr (REGS) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
+    int rbase = 0, rq0 = 0, rq1 = 0;
+    const double* rvb = nullptr;
+    int64_t rld = 0;
+    int rncols = kGroupCols;
+    const bool active = warp < prog.n_groups;
+    if (active) {
+      for (int g = 0; g < warp; ++g) rbase += kGroupCols * (groups[4 * (g + 1) + 3] - groups[4 * g + 3]);
+      const int4 gi = *reinterpret_cast<const int4*>(groups + 4 * warp);
+      rq0 = gi.w;
+      rq1 = groups[4 * (warp + 1) + 3];
+      rvb = in_ptr[gi.x] + gi.y;
+      rld = in_ld[gi.x];
+      rncols = gi.z;
+    }
+    // V values of iteration itx's row; the column indices come from the ring
+    auto load_v = [&](int itx, double (&v)[kCols][9]) {
+#ifdef SGK_P_NOV
+      if (itx > 0) return;
+#endif
+      mbar_wait(&bar_coef[itx & (kRing - 1)], (itx >> 2) & 1);
+      const int64_t row = r_begin + (int64_t)itx * r_step;
+      const int32_t* cg = reinterpret_cast<const int32_t*>(ring + (itx & (kRing - 1)) * slot_bytes + slot_bytes - 64) +
+                          (int)(((reinterpret_cast<uintptr_t>(pat.colind9) + (uintptr_t)row * 36) & 15) >> 2);
+      if (rncols == kGroupCols) {  // common case: immediate column offsets
+        const double* b = rvb + lane;
+#pragma unroll
+        for (int jj = 0; jj < 9; ++jj) {
+          const double* vr = b + (int64_t)cg[jj] * rld;
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) v[c][jj] = SGK_VLD(vr + 32 * c);
+        }
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 9; ++jj) {
+          const double* vr = rvb + (int64_t)cg[jj] * rld;
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) v[c][jj] = SGK_VLD(vr + min(32 * c + lane, rncols - 1));
+        }
+      }
+    };
+    // products of iteration it from the V registers v, handed to the consumers
+    auto body = [&](int it, const double (&v)[kCols][9]) {
+      const int cb = it & 1;
+      if (it >= 2) mbar_wait(&bar_empty[cb], ((it >> 1) & 1) ^ 1);  // consumers are done with U buffer cb (row it-2)
+      if (active) {
+        mbar_wait(&bar_coef[it & (kRing - 1)], (it >> 2) & 1);
+        const double* crow = reinterpret_cast<const double*>(ring + (it & (kRing - 1)) * slot_bytes);
+        double* ubq = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ubuf) + cb * ustride) + rbase;
+        int recn = rq0 < rq1 ? steps[rq0] : 0;
+        double2 p01 = make_double2(0.0, 0.0), p23 = p01;
+        if (rq0 < rq1) {
+          const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (recn & 0xFFFF));
+          p01 = a2[0];
+          p23 = a2[1];
+        }
+        for (int q = rq0; q < rq1; ++q, ubq += kGroupCols) {
+          const int rec = recn;
+          double* ub = ubq + (lane ^ (rec >> 16));
+          double a[10];
+          a[0] = p01.x; a[1] = p01.y; a[2] = p23.x; a[3] = p23.y;
+          {
+            const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (rec & 0xFFFF));
+#pragma unroll
+            for (int k = 2; k < 5; ++k) {
+              const double2 p = a2[k];
+              a[2 * k] = p.x;
+              a[2 * k + 1] = p.y;
+            }
+          }
+          recn = steps[q + 1 < rq1 ? q + 1 : q];
+          {
+            const double2* a2 = reinterpret_cast<const double2*>(crow + 10 * (recn & 0xFFFF));
+            p01 = a2[0];
+            p23 = a2[1];
+          }
+#ifdef SGK_P_NOSTS
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) {
+            const double u = dot9(a, v[c]);
+            if (u == 1.2345e-300) ub[32 * c] = u;
+          }
+#else
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) ub[32 * c] = dot9(a, v[c]);
+#endif
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_full[cb]);  // U buffer cb holds row it
+    };
+    double rv[kCols][9];
+    if (active && n_it > 0) load_v(0, rv);
+    for (int it = 0; it < n_it; ++it) {
+      body(it, rv);
+      if (active && it + 1 < n_it) load_v(it + 1, rv);  // prefetch: overlaps the next waits
+    }
+  } else {
+    if constexpr (REGS) asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+    const int cw = warp - NPW;
+    if (tid == kIssuer)
+      for (int itx = 0; itx < kRing && itx < n_it; ++itx) issue_row(itx);
+    int ocol[MAXOUT];
+#pragma unroll
+    for (int r = 0; r < MAXOUT; ++r) {
+      const int chunk = cw + r * 8;
+      ocol[r] = chunk < n_chunks ? __ldg(prog.out_col + chunk * 32 + lane) : -1;
+    }
+    for (int it = 0; it < n_it; ++it) {
+      const int cb = it & 1;
+      const int64_t row = r_begin + (int64_t)it * r_step;
+      mbar_wait(&bar_full[cb], (it >> 1) & 1);  // products of this row are in U buffer cb
+      // every producer is past row it: its ring slot is free for row it + kRing
+      if (tid == kIssuer && it + kRing < n_it) issue_row(it + kRing);
+      const unsigned char* smb = sm + cb * ustride;  // U addresses of buffer cb
+      double* orow = nullptr;
+      const double* irow = nullptr;
+      if constexpr (ONEOUT) {
+        orow = out.v[0].ptr + row * out.v[0].ld + out.v[0].col0;
+        if (init.v[0].ptr != nullptr) irow = init.v[0].ptr + row * init.v[0].ld + init.v[0].col0;
+      }
+#pragma unroll
+      for (int rb = 0; rb < MAXOUT; ++rb) {
+        const int chunk = cw + rb * 8;
+        if (chunk >= n_chunks) break;
+        const int npair = ccnt[chunk] >> 1;
+        const uint2* gp = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll kGatherUnroll
+        for (int e = 0; e < npair; ++e, gp += 32) {
+          const uint2 w = *gp;
+#ifdef SGK_P_NOCOEF
+          acc0 += *reinterpret_cast<const double*>(smb + (w.x >> 14));
+          acc1 += *reinterpret_cast<const double*>(smb + (w.y >> 14));
+#else
+          acc0 = fma(*reinterpret_cast<const double*>(sm + (w.x & 0x3FFF)),
+                     *reinterpret_cast<const double*>(smb + (w.x >> 14)), acc0);
+          acc1 = fma(*reinterpret_cast<const double*>(sm + (w.y & 0x3FFF)),
+                     *reinterpret_cast<const double*>(smb + (w.y >> 14)), acc1);
+#endif
+        }
+        const int oc = ocol[rb];
+        if (oc >= 0) {
+          const double acc = acc0 + acc1;
+          if constexpr (ONEOUT) {
+            double y = alpha.s[0] * acc;
+            if (irow != nullptr) y = fma(beta.s[0], irow[oc], y);
+            orow[oc] = y;
+          } else {
+            const int o = oc >> 24, k = oc & 0xFFFFFF;
+            const double al = sel4(alpha.s[0], alpha.s[1], alpha.s[2], alpha.s[3], o);
+            const double be = sel4(beta.s[0], beta.s[1], beta.s[2], beta.s[3], o);
+            const double* ip = sel4(init.v[0].ptr, init.v[1].ptr, init.v[2].ptr, init.v[3].ptr, o);
+            const int64_t il = sel4(init.v[0].ld, init.v[1].ld, init.v[2].ld, init.v[3].ld, o);
+            const int ic = sel4(init.v[0].col0, init.v[1].col0, init.v[2].col0, init.v[3].col0, o);
+            double* op = sel4(out.v[0].ptr, out.v[1].ptr, out.v[2].ptr, out.v[3].ptr, o);
+            const int64_t ol = sel4(out.v[0].ld, out.v[1].ld, out.v[2].ld, out.v[3].ld, o);
+            const int occ = sel4(out.v[0].col0, out.v[1].col0, out.v[2].col0, out.v[3].col0, o);
+            double y = al * acc;
+            if (ip != nullptr) y += be * ip[row * il + ic + k];
+            op[row * ol + occ + k] = y;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_empty[cb]);  // done reading U buffer cb
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Grid variant of the warp-specialised kernel (config-4 matvec): the pattern
 // is the Q1 9-point stencil of an nx x ny grid in natural order, so the
 // neighbours of node p = iy*nx + ix are p + dy*nx + dx and the producers
@@ -1058,6 +1361,57 @@ static int launch9ws(const sgk_pattern9& pat, const sgk_program9& prog, const Vi
   return check_launch("stencil9_ws_kernel");
 }
 
+template <int MAXOUT, bool ONEOUT, int NPW>
+static int launch9tma(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
+                      const ViewSet& init, const ScalarSet& a, const ScalarSet& b, cudaStream_t st) {
+  const size_t total = smem9_tma_total(pat.n_slices, prog);
+  constexpr int threads = (NPW + 8) * 32;
+  static bool attr_set = false;
+  if (!attr_set) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, stencil9_tma_kernel<MAXOUT, ONEOUT, NPW>);
+    cudaFuncSetAttribute(stencil9_tma_kernel<MAXOUT, ONEOUT, NPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         optin - (int)fa.sharedSizeBytes);
+    cudaGetLastError();
+    attr_set = true;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_tma_kernel<MAXOUT, ONEOUT, NPW>, threads, total);
+  if (occ < 1) return SGK_ELIMIT;
+  int64_t grid = (int64_t)sm_count() * occ;
+  if (grid > pat.n_rows) grid = pat.n_rows;
+  if (grid < 1) return SGK_OK;
+  static const bool dbg = getenv("SGKKT_S9_DEBUG") != nullptr;
+  if (dbg)
+    fprintf(stderr, "stencil9_tma_kernel<%d,%d,%d>: smem %zu B, grid %d, rows %d, groups %d, chunks %d\n", MAXOUT,
+            (int)ONEOUT, NPW, total, (int)grid, pat.n_rows, prog.n_groups, prog.n_chunks);
+  stencil9_tma_kernel<MAXOUT, ONEOUT, NPW><<<(int)grid, threads, total, st>>>(pat, prog, in, out, init, a, b);
+  return check_launch("stencil9_tma_kernel");
+}
+
+// TMA/mbarrier pipeline for resident product-heavy programs: 6..8 column
+// groups (8 producer warps) or 9..12 (12 producer warps); 8 consumer warps
+// share the output chunks.  SGK_ELIMIT when it does not apply or fit.
+template <int NPW>
+static int launch9tma_any(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
+                          const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int n_out, cudaStream_t st) {
+  const int per = (prog.n_chunks + 7) / 8;
+#define SGK_TMA_CASE(M)                                                                         \
+  if (per <= M)                                                                                 \
+    return n_out == 1 ? launch9tma<M, true, NPW>(pat, prog, in, out, init, a, b, st)            \
+                      : launch9tma<M, false, NPW>(pat, prog, in, out, init, a, b, st);
+  SGK_TMA_CASE(1)
+  SGK_TMA_CASE(2)
+  SGK_TMA_CASE(4)
+  SGK_TMA_CASE(8)
+  SGK_TMA_CASE(16)
+#undef SGK_TMA_CASE
+  return SGK_ELIMIT;
+}
+
 template <int MAXOUT, bool RESIDENT, bool ONEOUT, bool BIG>
 static int launch9r(const sgk_pattern9& pat, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
                     const ViewSet& init, const ScalarSet& a, const ScalarSet& b, int threads, cudaStream_t st) {
@@ -1102,6 +1456,18 @@ static int launch9(const sgk_pattern9& pat, const sgk_program9& prog, const View
     return v ? atoi(v) : -1;
   }();
   const bool ws = ws_env < 0 ? prog.n_groups >= 6 : ws_env != 0;
+  // SGKKT_S9_TMA=0 falls back to the named-barrier / alternating kernels
+  static const int tma_env = [] {
+    const char* v = getenv("SGKKT_S9_TMA");
+    return v ? atoi(v) : 1;
+  }();
+  if (tma_env && ws && res) {
+    int rc = SGK_ELIMIT;
+    if (threads == 256 && prog.n_groups <= 8) rc = launch9tma_any<8>(pat, prog, in, out, init, a, b, n_out, st);
+    else if (threads > 256 && prog.n_groups > 8 && prog.n_groups <= 12)
+      rc = launch9tma_any<12>(pat, prog, in, out, init, a, b, n_out, st);
+    if (rc != SGK_ELIMIT) return rc;
+  }
   if (ws && res && threads == 256 && prog.n_groups <= 8) {
     const int rc = n_out == 1 ? launch9ws<MAXOUT, true>(pat, prog, in, out, init, a, b, st)
                               : launch9ws<MAXOUT, false>(pat, prog, in, out, init, a, b, st);
