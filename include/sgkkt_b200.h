@@ -305,6 +305,15 @@ typedef struct {
   int32_t dense_r0;           /* first row of the dense region              */
   int32_t dense_pad;
   const double* dense;        /* off-diagonal region blocks (sgk_trigroups) */
+  /* column-panel form (pcol != NULL; linalg.wide_panels): tile_seg holds the
+   * panel range of each tile; a panel is 32 distinct solution rows (pcol)
+   * against a dense zero-filled 32 x 32 block pval[panel][group row][column];
+   * a slotted tile writes the partial sums of all group rows to part slots
+   * tile_slot[tile] + row-in-group (-1: not slotted).  The seg_* arrays are
+   * unused in this form.                                                    */
+  const int32_t* pcol;        /* [32 * n_panels] processing-space columns    */
+  const double* pval;         /* [1024 * n_panels]                           */
+  const int32_t* tile_slot;   /* [n_tiles]                                   */
 } sgk_triwide;
 
 /* Chunk width (columns per task) the wide solve uses for `width`.          */

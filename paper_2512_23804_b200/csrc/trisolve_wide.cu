@@ -66,7 +66,7 @@ __device__ __forceinline__ unsigned long long triw_timer() {
 #define TRIW_TR(k) do {} while (0)
 #endif
 
-template <bool FWD, int CPL>
+template <bool FWD, int CPL, bool PANEL>
 __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview io, double* __restrict__ work,
                                                   double* __restrict__ part, int width, int ldw, int n_chunks,
                                                   int epoch) {
@@ -320,6 +320,90 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
       // tasks that always finalise load their group's B rows up front (static)
       const bool b_early = kind == 2 || (nt == 1 && !dgrp);
       if (b_early) init_b();
+      if constexpr (PANEL) {
+        // column-panel tile: per panel the 32 distinct solution rows and the
+        // dense 32 x 32 coefficient block are staged in shared memory once and
+        // every warp accumulates two group rows (rows 2w, 2w+1; lanes CPL
+        // columns each): a solution row is read once per (group, panel)
+        auto stage_vals = [&](int pi) {
+          const double* pv = t.pval + (int64_t)WG * WG * pi;
+          for (int i = tid; i < WG * WG; i += blockDim.x) lg[i / WG][i % WG] = __ldg(pv + i);
+        };
+        if (s0 < s1) stage_vals(s0);  // static: before the dependency wait
+        if (warp == 0) {
+          const int da = __ldg(t.tile_dep_ptr + tile), db = __ldg(t.tile_dep_ptr + tile + 1);
+          for (int d = da + lane; d < db; d += 32) {
+            const int32_t* fl = t.flags + (int64_t)__ldg(t.tile_dep + d) * n_chunks + chunk;
+            while (ld_relaxed(fl) != epoch) __nanosleep(32);
+          }
+          fence_acq_rel();
+        }
+        __syncthreads();
+        TRIW_TR(1);
+        double dacc[2][CPL];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) dacc[q][k] = 0.0;
+        for (int pi = s0; pi < s1; ++pi) {
+          for (int i = tid; i < WG * CH; i += blockDim.x) {
+            const int k = i / CH, c = i - k * CH;
+            const int src = __ldg(t.pcol + WG * pi + k);
+            const int wr = t.reversed ? t.n - 1 - src : src;
+            sp[k][c] = __ldcg(work + (int64_t)wr * ldw + c0 + c);
+          }
+          if (pi > s0) stage_vals(pi);
+          __syncthreads();
+#pragma unroll 4
+          for (int k = 0; k < WG; ++k) {
+            double xk[CPL];
+#pragma unroll
+            for (int kk = 0; kk < CPL; ++kk) xk[kk] = sp[k][CPL * lane + kk];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const double d = lg[2 * warp + q][k];
+#pragma unroll
+              for (int kk = 0; kk < CPL; ++kk) dacc[q][kk] = fma(d, xk[kk], dacc[q][kk]);
+            }
+          }
+          __syncthreads();
+        }
+        TRIW_TR(2);
+        if (kind == 2 || (nt == 1 && !dgrp)) {
+          // finalising tile: P = B (prefetched) - own sums (- the other tiles' slots)
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int kk = 0; kk < CPL; ++kk) pr[2 * warp + q][CPL * lane + kk] -= dacc[q][kk];
+          if (kind == 2) {
+            if (tid == 0) {
+              const int32_t* cnt = t.counters + (int64_t)gi * n_chunks + chunk;
+              while (ld_relaxed(cnt) != nt - 1) __nanosleep(32);
+            }
+            __syncthreads();
+            fence_acq_rel();
+            TRIW_TR(3);
+            sub_slots();
+          }
+        } else {
+          // slotted tile: the sums of every group row -> part slots; count in
+          const int slot0 = __ldg(t.tile_slot + tile);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int r = 2 * warp + q;
+            if (r < g) {
+              double* ps = part + (int64_t)(slot0 + r) * ldw + c0 + CPL * lane;
+#pragma unroll
+              for (int kk = 0; kk < CPL; ++kk) __stcg(ps + kk, dacc[q][kk]);
+            }
+          }
+          __threadfence();
+          __syncthreads();
+          if (tid == 0) atomicAdd(t.counters + (int64_t)gi * n_chunks + chunk, 1);
+          TRIW_TR(3);
+          continue;
+        }
+      } else {
       for (int i = tid; i < s1 - s0; i += blockDim.x) {
         s_row[i] = __ldg(t.seg_row + s0 + i);
         s_e0[i] = __ldg(t.seg_e0 + s0 + i);
@@ -421,6 +505,7 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
         // 2: one-tile group: P = B (prefetched) - segment sums of each row
         sub_runs();
       }
+      }  // !PANEL
     }
     if (!minv_early) load_minv();
     __syncthreads();
@@ -466,7 +551,7 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
   }
 }
 
-template <int CPL>
+template <int CPL, bool PANEL>
 static int launch_wide_t(const sgk_triwide& L, const sgk_triwide& U, const sgk_segview& b, const sgk_segview& x,
                          double* work, double* part, int width, int epoch, cudaStream_t st) {
   constexpr int CH = 32 * CPL;
@@ -475,13 +560,13 @@ static int launch_wide_t(const sgk_triwide& L, const sgk_triwide& U, const sgk_s
   const size_t dyn = sizeof(double) * (size_t)(WSMAX + WG) * CH;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(trsv_wide<true, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    cudaFuncSetAttribute(trsv_wide<false, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaFuncSetAttribute(trsv_wide<true, CPL, PANEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaFuncSetAttribute(trsv_wide<false, CPL, PANEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     cudaGetLastError();
     attr_set = true;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_wide<true, CPL>, 32 * WW, dyn);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_wide<true, CPL, PANEL>, 32 * WW, dyn);
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)sm_count() * occ;
   const int64_t tasks = (int64_t)std::max(L.n_tiles, U.n_tiles) * n_chunks;
@@ -491,10 +576,10 @@ static int launch_wide_t(const sgk_triwide& L, const sgk_triwide& U, const sgk_s
   cudaMemsetAsync(U.ticket, 0, sizeof(int32_t), st);
   cudaMemsetAsync(L.counters, 0, sizeof(int32_t) * (size_t)L.n_groups * n_chunks, st);
   cudaMemsetAsync(U.counters, 0, sizeof(int32_t) * (size_t)U.n_groups * n_chunks, st);
-  trsv_wide<true, CPL><<<(int)grid, 32 * WW, dyn, st>>>(L, b, work, part, width, ldw, n_chunks, epoch);
+  trsv_wide<true, CPL, PANEL><<<(int)grid, 32 * WW, dyn, st>>>(L, b, work, part, width, ldw, n_chunks, epoch);
   int rc = check_launch("trsv_wide<fwd>");
   if (rc) return rc;
-  trsv_wide<false, CPL><<<(int)grid, 32 * WW, dyn, st>>>(U, x, work, part, width, ldw, n_chunks, epoch);
+  trsv_wide<false, CPL, PANEL><<<(int)grid, 32 * WW, dyn, st>>>(U, x, work, part, width, ldw, n_chunks, epoch);
   return check_launch("trsv_wide<bwd>");
 }
 
@@ -520,9 +605,16 @@ extern "C" int sgk_trisolve_wide(const sgk_triwide* L, const sgk_triwide* U, con
   if (L->n == 0 || width == 0) return SGK_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int ch = sgk_trisolve_wide_chunk_cols(width);
-  if (ch == 128) return launch_wide_t<4>(*L, *U, *b, *x, work, part, width, epoch, st);
-  if (ch == 64) return launch_wide_t<2>(*L, *U, *b, *x, work, part, width, epoch, st);
-  return launch_wide_t<1>(*L, *U, *b, *x, work, part, width, epoch, st);
+  const bool panel = L->pcol != nullptr;
+  SGK_REQUIRE(panel == (U->pcol != nullptr), "sgk_trisolve_wide: L and U must use the same tile form");
+  SGK_REQUIRE(!panel || (L->pval && U->pval && L->tile_slot && U->tile_slot), "sgk_trisolve_wide: panel arrays not set");
+  if (panel) {
+    if (ch == 64) return launch_wide_t<2, true>(*L, *U, *b, *x, work, part, width, epoch, st);
+    return launch_wide_t<1, true>(*L, *U, *b, *x, work, part, width, epoch, st);
+  }
+  if (ch == 128) return launch_wide_t<4, false>(*L, *U, *b, *x, work, part, width, epoch, st);
+  if (ch == 64) return launch_wide_t<2, false>(*L, *U, *b, *x, work, part, width, epoch, st);
+  return launch_wide_t<1, false>(*L, *U, *b, *x, work, part, width, epoch, st);
 }
 
 #ifdef SGK_TRIW_TRACE

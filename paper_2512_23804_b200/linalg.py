@@ -13,6 +13,7 @@ SuperLU convention (verified in tests/test_linalg_host.py):
 from __future__ import annotations
 
 import ctypes
+import os as _os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -355,17 +356,116 @@ def wide_tiles(strict: csr_matrix, gptr: np.ndarray, order: np.ndarray, dense: t
                 seg_e1=seg_e1, seg_slot=np.asarray(seg_slot, np.int64), row_slot_ptr=rs_ptr, row_slot=rs)
 
 
+# SGKKT_TRIW_PANEL=1: the column-panel form of the wide solve (A/B; measured slower, see DESIGN K3)
+WIDE_PANELS = _os.environ.get("SGKKT_TRIW_PANEL", "0") != "0"
+PANEL_COLS = 32       # distinct solution rows per panel (= WG in csrc/trisolve_wide.cu)
+PANELS_PER_TILE = 4   # panels per tile: a heavy group spreads over ceil(panels / 4) CTAs per chunk
+
+
+def wide_panels(strict: csr_matrix, gptr: np.ndarray, order: np.ndarray, dense: tuple[int, int] = (0, 0),
+                panels_per_tile: int = PANELS_PER_TILE):
+    """Column-panel form of the wide-RHS solve (csrc/trisolve_wide.cu, PANEL):
+    a group's outside entries (columns before the group; for rows of a dense
+    region, before the region) are regrouped by DISTINCT column: every run of
+    <= PANEL_COLS sorted distinct columns is a panel, stored as a dense
+    zero-filled PANEL_COLS x PANEL_COLS block (group row x panel column), so a
+    solution row is read once per (group, panel) instead of once per entry
+    (SuperLU's triangles are supernodal: config-5 P~ has 11 entries per
+    distinct (group, column) pair).  Tiles hold <= panels_per_tile panels of
+    one group; tile kinds, part slots (one per (slotted tile, group row)) and
+    the dense task follow wide_tiles.  Returns a dict of host arrays."""
+    n = strict.shape[0]
+    ng = len(gptr) - 1
+    ip, ix, dat = strict.indptr.astype(np.int64), strict.indices.astype(np.int64), strict.data
+    gid = np.repeat(np.arange(ng), np.diff(gptr))
+    d0, d1 = dense
+    pcol, pval = [], []
+    tile_group, tile_pan, tile_kind, tile_slot = [], [0], [], []
+    dep_list = []
+    group_ntiles = np.zeros(ng, np.int64)
+    row_slots = [[] for _ in range(n)]
+    n_slots = 0
+    n_pan = 0
+    for g in order:
+        a, b = int(gptr[g]), int(gptr[g + 1])
+        is_dense = d1 > d0 and d0 <= a < d1
+        left = d0 if is_dense else a
+        e0, e1 = int(ip[a]), int(ip[b])
+        cols = ix[e0:e1]
+        keep = cols < left
+        cols = cols[keep]
+        rows = np.repeat(np.arange(a, b), np.diff(ip[a:b + 1]))[keep] - a
+        vals = dat[e0:e1][keep]
+        ucols, inv = np.unique(cols, return_inverse=True)
+        npan = (len(ucols) + PANEL_COLS - 1) // PANEL_COLS
+        if npan:
+            blk = np.zeros((npan, PANEL_COLS, PANEL_COLS))
+            blk[inv // PANEL_COLS, rows, inv % PANEL_COLS] = vals
+            pc = np.empty(npan * PANEL_COLS, np.int64)
+            pc[: len(ucols)] = ucols
+            # padding columns re-read the panel's first column (a finished dependency) against zeros
+            pc[len(ucols):] = ucols[(npan - 1) * PANEL_COLS]
+            pcol.append(pc)
+            pval.append(blk.reshape(-1))
+        ntile = (npan + panels_per_tile - 1) // panels_per_tile
+        if not is_dense:
+            ntile = max(ntile, 1)  # a group without outside entries is finalised by one empty tile
+        group_ntiles[g] = ntile
+        for ti in range(ntile):
+            p0 = ti * panels_per_tile
+            p1 = min(npan, p0 + panels_per_tile)
+            designated = ntile > 1 and not is_dense and ti == ntile - 1
+            slotted = (ntile > 1 or is_dense) and not designated
+            if slotted:
+                for r in range(b - a):
+                    row_slots[a + r].append(n_slots + r)
+                tile_slot.append(n_slots)
+                n_slots += b - a
+            else:
+                tile_slot.append(-1)
+            tile_group.append(int(g))
+            tile_pan.append(n_pan + p1)
+            tile_kind.append(2 if designated else 0)
+            dep_list.append(np.unique(gid[ucols[p0 * PANEL_COLS: p1 * PANEL_COLS]]) if npan else np.zeros(0, np.int64))
+        n_pan += npan
+        if is_dense:
+            tile_group.append(int(g))
+            tile_pan.append(n_pan)
+            tile_kind.append(1)
+            tile_slot.append(-1)
+            dep_list.append(np.zeros(0, np.int64))
+    n_tiles = len(tile_group)
+    dep_ptr = np.concatenate([[0], np.cumsum([len(d) for d in dep_list])]).astype(np.int64)
+    dep = np.concatenate(dep_list) if dep_list else np.zeros(0, np.int64)
+    rs_ptr = np.concatenate([[0], np.cumsum([len(r) for r in row_slots])]) if n else np.zeros(1, np.int64)
+    rs = np.asarray([q for r in row_slots for q in r], np.int64)
+    return dict(n_tiles=n_tiles, n_slots=n_slots, n_panels=n_pan, tile_group=np.asarray(tile_group, np.int64),
+                tile_seg=np.asarray(tile_pan, np.int64), tile_kind=np.asarray(tile_kind, np.int64),
+                tile_slot=np.asarray(tile_slot, np.int64), dep_ptr=dep_ptr, dep=dep, group_ntiles=group_ntiles,
+                pcol=np.concatenate(pcol) if pcol else np.zeros(0, np.int64),
+                pval=np.concatenate(pval) if pval else np.zeros(0), row_slot_ptr=rs_ptr, row_slot=rs)
+
+
 def _wide(strict: csr_matrix, grouped_bufs, st_grouped, work_row, io_row):
     """sgk_triwide for one processing-space triangle, sharing the grouped
     form's CSR, group pointer, row maps and dense inverses."""
     gptr, order, mptr_buf, minv_buf = st_grouped._host
     g = st_grouped
     dense = (g.dense_r0, g.dense_r0 + DENSE_BLOCK * g.dense_nb) if g.dense_nb else (0, 0)
-    w = wide_tiles(strict, gptr, order, dense)
     i32 = lambda a: _i32(a if len(a) else [0])
+    panel = WIDE_PANELS
+    if panel:
+        w = wide_panels(strict, gptr, order, dense)
+        zero = i32([0])
+        seg = [zero, zero, zero, zero]
+        extra = [i32(w["pcol"]), _f64(w["pval"] if len(w["pval"]) else [0.0]), i32(w["tile_slot"])]
+    else:
+        w = wide_tiles(strict, gptr, order, dense)
+        seg = [i32(w["seg_row"]), i32(w["seg_e0"]), i32(w["seg_e1"]), i32(w["seg_slot"])]
+        extra = []
     bufs = [i32(w["tile_group"]), i32(w["tile_seg"]), i32(w["dep_ptr"]), i32(w["dep"]), i32(w["group_ntiles"]),
-            i32(w["seg_row"]), i32(w["seg_e0"]), i32(w["seg_e1"]), i32(w["seg_slot"]), i32(w["row_slot_ptr"]),
-            i32(w["row_slot"]), torch.zeros(1, dtype=torch.int32, device=device()), i32(w["tile_kind"])]
+            seg[0], seg[1], seg[2], seg[3], i32(w["row_slot_ptr"]),
+            i32(w["row_slot"]), torch.zeros(1, dtype=torch.int32, device=device()), i32(w["tile_kind"])] + extra
     st = _lib.TriWide(
         n=g.n, n_groups=g.n_groups, n_tiles=w["n_tiles"], reversed=g.reversed, rowptr=g.rowptr,
         colind=g.colind, vals=g.vals, group_ptr=g.group_ptr, tile_group=bufs[0].data_ptr(),
@@ -376,6 +476,8 @@ def _wide(strict: csr_matrix, grouped_bufs, st_grouped, work_row, io_row):
         minv=minv_buf.data_ptr(), flags=None, counters=None, ticket=bufs[11].data_ptr(),
         tile_kind=bufs[12].data_ptr(), dense_g0=g.dense_g0, dense_nb=g.dense_nb, dense_r0=g.dense_r0,
         dense_pad=0, dense=g.dense,
+        pcol=extra[0].data_ptr() if panel else None, pval=extra[1].data_ptr() if panel else None,
+        tile_slot=extra[2].data_ptr() if panel else None,
     )
     return st, bufs, w["n_slots"]
 

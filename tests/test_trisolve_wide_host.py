@@ -159,3 +159,130 @@ def test_wide_tiles_with_dense_region_groups():
     assert dense[1] - dense[0] >= 64
     w = _check(strict, None, dense=dense)
     assert int(np.sum(w["tile_kind"] == 1)) == (dense[1] - dense[0]) // linalg.DENSE_BLOCK
+
+
+# ---- column-panel form (linalg.wide_panels, trsv_wide<PANEL>) -----------------
+
+def _emulate_panels(strict, gptr, dinv, w, b, dense=(0, 0)):
+    """The PANEL kernel's arithmetic, tile by tile in ticket order."""
+    mptr, minv = linalg.group_inverses(strict, gptr, dinv)
+    x = np.full_like(b, np.nan)
+    part = np.full((max(1, w["n_slots"]), b.shape[1]), np.nan)
+    done_tiles = {}
+    tp = w["tile_seg"]
+    d0, d1 = dense
+    dblk = linalg.dense_blocks(strict, dense) if d1 > d0 else None
+    pc = w["pcol"].reshape(-1, linalg.PANEL_COLS)
+    pv = w["pval"].reshape(-1, linalg.PANEL_COLS, linalg.PANEL_COLS)
+
+    def minus_slots(p_rows, a, bb):
+        for r in range(a, bb):
+            for q in range(w["row_slot_ptr"][r], w["row_slot_ptr"][r + 1]):
+                p_rows[r - a] -= part[w["row_slot"][q]]
+
+    for t in range(w["n_tiles"]):
+        g = int(w["tile_group"][t])
+        a, bb = int(gptr[g]), int(gptr[g + 1])
+        g_n = bb - a
+        nt = int(w["group_ntiles"][g])
+        is_dense = d1 > d0 and d0 <= a < d1
+        kind = int(w["tile_kind"][t])
+        if kind == 1:
+            assert done_tiles.get(g, 0) == nt
+            bi = (a - d0) // linalg.DENSE_BLOCK
+            p_rows = b[a:bb].copy()
+            minus_slots(p_rows, a, bb)
+            if bi:
+                off = linalg.DENSE_BLOCK ** 2 * bi * (bi - 1) // 2
+                blk = dblk[off:off + linalg.DENSE_BLOCK * linalg.DENSE_BLOCK * bi].reshape(linalg.DENSE_BLOCK, -1)
+                p_rows -= blk @ x[d0:a]
+        else:
+            acc = np.zeros((linalg.PANEL_COLS, b.shape[1]))
+            for pi in range(tp[t], tp[t + 1]):
+                xs = x[pc[pi]]
+                assert np.all(np.isfinite(xs)), "panel reads an unfinished row"
+                acc += pv[pi] @ xs
+            assert np.all(acc[g_n:] == 0.0)
+            if kind == 2 or (nt == 1 and not is_dense):
+                p_rows = b[a:bb] - acc[:g_n]
+                if kind == 2:
+                    assert done_tiles.get(g, 0) == nt - 1
+                    minus_slots(p_rows, a, bb)
+            else:
+                s0 = int(w["tile_slot"][t])
+                assert s0 >= 0
+                part[s0:s0 + g_n] = acc[:g_n]
+                done_tiles[g] = done_tiles.get(g, 0) + 1
+                continue
+        mi = minv[mptr[g]:mptr[g] + g_n * g_n].reshape(g_n, g_n)
+        x[a:bb] = mi @ p_rows
+    return x
+
+
+def _check_panels(strict, dinv, dense=(0, 0), panels_per_tile=2):
+    gptr, order, _ = linalg.chain_groups(strict, dense=dense)
+    w = linalg.wide_panels(strict, gptr, order, dense, panels_per_tile=panels_per_tile)
+    n = strict.shape[0]
+    # the panels hold every outside entry exactly once and nothing else
+    gid = np.repeat(np.arange(len(gptr) - 1), np.diff(gptr))
+    row_of = np.repeat(np.arange(n), np.diff(strict.indptr))
+    left = gptr[gid[row_of]]
+    if dense[1] > dense[0]:
+        left = np.where((row_of >= dense[0]) & (row_of < dense[1]), dense[0], left)
+    outside = strict.indices < left
+    want_sum = sp.csr_matrix((strict.data[outside], (row_of[outside], strict.indices[outside])), shape=(n, n))
+    rec = sp.lil_matrix((n, n))
+    pc = w["pcol"].reshape(-1, linalg.PANEL_COLS)
+    pv = w["pval"].reshape(-1, linalg.PANEL_COLS, linalg.PANEL_COLS)
+    tp = w["tile_seg"]
+    assert np.all(np.diff(tp) <= panels_per_tile)
+    for t in range(w["n_tiles"]):
+        a = int(gptr[int(w["tile_group"][t])])
+        for pi in range(tp[t], tp[t + 1]):
+            r, k = np.nonzero(pv[pi])
+            for rr, kk in zip(r, k):
+                assert rec[a + rr, pc[pi, kk]] == 0.0
+                rec[a + rr, pc[pi, kk]] = pv[pi, rr, kk]
+    assert abs(rec.tocsr() - want_sum).max() == 0.0
+    # every group is finalised by exactly one task, dependencies by earlier tickets
+    first_tile, last_tile = {}, {}
+    for t, g in enumerate(w["tile_group"]):
+        first_tile.setdefault(int(g), t)
+        last_tile[int(g)] = t
+    assert len(first_tile) == len(gptr) - 1
+    for t in range(w["n_tiles"]):
+        for d in w["dep"][w["dep_ptr"][t]:w["dep_ptr"][t + 1]]:
+            assert last_tile[int(d)] < first_tile[int(w["tile_group"][t])]
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal((n, 5))
+    x = _emulate_panels(strict, gptr, dinv, w, b, dense)
+    full = strict.toarray()
+    full[np.arange(n), np.arange(n)] = 1.0 if dinv is None else 1.0 / np.asarray(dinv)
+    want = solve_triangular(full, b, lower=True)
+    assert np.abs(x - want).max() <= 1e-11 * np.abs(want).max()
+    return w
+
+
+def test_wide_panels_unit_lower():
+    w = _check_panels(_strict_lower(300, 0.05, 1), None)
+    assert w["n_panels"] >= 1
+
+
+def test_wide_panels_heavy_groups_split_over_tiles():
+    strict = _strict_lower(400, 0.02, 2, dense_tail=96)
+    dinv = 1.0 / (1.0 + np.random.default_rng(5).random(400))
+    w = _check_panels(strict, dinv)
+    assert int(w["group_ntiles"].max()) > 1 and w["n_slots"] > 0
+
+
+def test_wide_panels_with_dense_region_groups():
+    strict = _strict_lower(512, 0.01, 4, dense_tail=160)
+    dense = linalg.dense_region(strict)
+    w = _check_panels(strict, None, dense=dense)
+    assert int(np.sum(w["tile_kind"] == 1)) == (dense[1] - dense[0]) // linalg.DENSE_BLOCK
+
+
+def test_wide_panels_group_without_outside_entries_gets_a_tile():
+    strict = sp.csr_matrix(np.tril(np.ones((40, 40)), k=-1) * 0.01)  # one chain: later groups depend on earlier
+    strict = sp.block_diag([strict, sp.csr_matrix((8, 8))], format="csr")  # 8 isolated rows
+    _check_panels(strict, None)
