@@ -314,6 +314,15 @@ typedef struct {
   const int32_t* pcol;        /* [32 * n_panels] processing-space columns    */
   const double* pval;         /* [1024 * n_panels]                           */
   const int32_t* tile_slot;   /* [n_tiles]                                   */
+  /* explicit inverse of the dense region's triangle (NULL: the region's
+   * blocks are streamed by the dense tasks): (32 dense_nb)^2 doubles,
+   * row-major, inv(strict + diagonal) of rows/columns [dense_r0, +32 dense_nb).
+   * The region is then solved by one blocked product around the sync-free
+   * kernel (before it for a leading region, after it for a trailing one);
+   * `part` needs 32 dense_nb extra rows after the part slots.               */
+  const double* region_inv;
+  int32_t part_rows;          /* part slots in use: the region's P rows start here */
+  int32_t region_pad;
 } sgk_triwide;
 
 /* Chunk width (columns per task) the wide solve uses for `width`.          */

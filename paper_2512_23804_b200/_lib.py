@@ -126,6 +126,7 @@ class TriWide(ctypes.Structure):
         ("io_row", c_vp), ("minv_ptr", c_vp), ("minv", c_vp), ("flags", c_vp), ("counters", c_vp),
         ("ticket", c_vp), ("tile_kind", c_vp), ("dense_g0", c_i32), ("dense_nb", c_i32), ("dense_r0", c_i32),
         ("dense_pad", c_i32), ("dense", c_vp), ("pcol", c_vp), ("pval", c_vp), ("tile_slot", c_vp),
+        ("region_inv", c_vp), ("part_rows", c_i32), ("region_pad", c_i32),
     ]
 
 

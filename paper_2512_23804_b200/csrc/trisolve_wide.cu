@@ -22,6 +22,7 @@
 // Deadlock freedom is the ticket argument of trsv_group: tiles are ordered
 // by group level, so a tile only waits for groups finalised by tiles with
 // earlier tickets, which are resident or done.
+#include <algorithm>
 #include <cstdlib>
 
 #include "sgk_common.cuh"
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
     const int c0 = chunk * CH;
     const int gi = __ldg(t.tile_group + tile);
     const int kind = __ldg(t.tile_kind + tile);
+    if (kind == 1 && t.region_inv != nullptr) continue;  // the region is solved by region_gemm
     const int s0 = __ldg(t.tile_seg + tile), s1 = __ldg(t.tile_seg + tile + 1);
     const int nt = __ldg(t.group_ntiles + gi);
     const int r0 = __ldg(t.group_ptr + gi), g = __ldg(t.group_ptr + gi + 1) - r0;
@@ -551,6 +553,108 @@ __global__ void __launch_bounds__(512, 1) trsv_wide(sgk_triwide t, sgk_segview i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dense region by explicit inverse (sgk_triwide.region_inv): the region's
+// triangle T (2560 / 3072 rows at config 5: the separator rows COLAMD orders
+// last) is inverted once on the host, so its solve is P = B - (part slots of
+// the entries left of the region), X = inv(T) P — one blocked lower-triangular
+// product with no dependency chain (the streamed form runs 80-96 sequential
+// 32-row block solves, ~11.7 us each).  A trailing region (L) runs after the
+// sync-free kernel, a leading one (reversed U) before it and publishes the
+// region groups' flags for the tiles that read them.
+template <bool FWD>
+__global__ void region_prep(sgk_triwide t, sgk_segview io, const double* __restrict__ work, double* __restrict__ part,
+                            int width, int ldw) {
+  const int64_t total = (int64_t)WG * t.dense_nb * ldw;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ldw), col = (int)(i - (int64_t)r * ldw);
+    const int p = t.dense_r0 + r;
+    double v = 0.0;
+    if (col < width) {
+      const double b = FWD ? *wseg_ptr(io, __ldg(t.io_row + p), col)
+                           : __ldcg(work + (int64_t)__ldg(t.work_row + p) * ldw + col);
+      double sum = 0.0;  // the row's part slots in tile order, as the streamed finaliser sums them
+      for (int q = __ldg(t.row_slot_ptr + p); q < __ldg(t.row_slot_ptr + p + 1); ++q)
+        sum += __ldcg(part + (int64_t)__ldg(t.row_slot + q) * ldw + col);
+      v = b - sum;
+    }
+    part[((int64_t)t.part_rows + r) * ldw + col] = v;
+  }
+}
+
+template <bool FWD, int CH>
+__global__ void __launch_bounds__(256) region_gemm(sgk_triwide t, sgk_segview io, double* __restrict__ work,
+                                                  const double* __restrict__ part, int width, int ldw, int n_chunks,
+                                                  int epoch) {
+  constexpr int TX = CH / 4, TY = 256 / TX, RPT = WG / TY;  // thread: RPT rows x 4 columns
+  __shared__ double as[WG][WG + 1];
+  __shared__ __align__(16) double ps[WG][CH];
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  const int bi = t.dense_nb - 1 - blockIdx.x;  // longest products first
+  const int chunk = blockIdx.y, c0 = chunk * CH;
+  const int m = WG * t.dense_nb;
+  const double* pd = part + (int64_t)t.part_rows * ldw + c0;
+  double acc[RPT][4];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[j][c] = 0.0;
+  for (int kb = 0; kb <= bi; ++kb) {
+    for (int i = tid; i < WG * WG; i += 256) {
+      const int r = i / WG, k = i - r * WG;
+      as[r][k] = __ldg(t.region_inv + (int64_t)(WG * bi + r) * m + WG * kb + k);
+    }
+    for (int i = tid; i < WG * CH / 2; i += 256) {
+      const int k = i / (CH / 2), c = 2 * (i - k * (CH / 2));
+      *reinterpret_cast<double2*>(&ps[k][c]) = __ldcg(reinterpret_cast<const double2*>(pd + (int64_t)(WG * kb + k) * ldw + c));
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < WG; ++k) {
+      const double2 p01 = *reinterpret_cast<const double2*>(&ps[k][4 * tx]);
+      const double2 p23 = *reinterpret_cast<const double2*>(&ps[k][4 * tx + 2]);
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const double a = as[ty + TY * j][k];
+        acc[j][0] = fma(a, p01.x, acc[j][0]);
+        acc[j][1] = fma(a, p01.y, acc[j][1]);
+        acc[j][2] = fma(a, p23.x, acc[j][2]);
+        acc[j][3] = fma(a, p23.y, acc[j][3]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int p = t.dense_r0 + WG * bi + ty + TY * j;
+    double* wrow = work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + 4 * tx;
+    const int iorow = __ldg(t.io_row + p);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int col = c0 + 4 * tx + c;
+      __stcg(wrow + c, col < width ? acc[j][c] : 0.0);
+      if (!FWD && col < width) *wseg_ptr(io, iorow, col) = acc[j][c];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    fence_acq_rel();
+    st_relaxed(t.flags + (int64_t)(t.dense_g0 + bi) * n_chunks + chunk, epoch);
+  }
+}
+
+template <bool FWD, int CH>
+static int launch_region(const sgk_triwide& t, const sgk_segview& io, double* work, double* part, int width, int ldw,
+                         int n_chunks, int epoch, cudaStream_t st) {
+  const int64_t total = (int64_t)WG * t.dense_nb * ldw;
+  const int pgrid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 8);
+  region_prep<FWD><<<pgrid, 256, 0, st>>>(t, io, work, part, width, ldw);
+  int rc = check_launch("region_prep");
+  if (rc) return rc;
+  region_gemm<FWD, CH><<<dim3(t.dense_nb, n_chunks), 256, 0, st>>>(t, io, work, part, width, ldw, n_chunks, epoch);
+  return check_launch("region_gemm");
+}
+
 template <int CPL, bool PANEL>
 static int launch_wide_t(const sgk_triwide& L, const sgk_triwide& U, const sgk_segview& b, const sgk_segview& x,
                          double* work, double* part, int width, int epoch, cudaStream_t st) {
@@ -576,11 +680,20 @@ static int launch_wide_t(const sgk_triwide& L, const sgk_triwide& U, const sgk_s
   cudaMemsetAsync(U.ticket, 0, sizeof(int32_t), st);
   cudaMemsetAsync(L.counters, 0, sizeof(int32_t) * (size_t)L.n_groups * n_chunks, st);
   cudaMemsetAsync(U.counters, 0, sizeof(int32_t) * (size_t)U.n_groups * n_chunks, st);
+  // an inverted dense region: before the sync-free kernel when it leads the triangle, after it when it trails
+  const bool l_reg = L.region_inv != nullptr && L.dense_nb > 0, u_reg = U.region_inv != nullptr && U.dense_nb > 0;
+  int rc = SGK_OK;
+  if (l_reg && L.dense_r0 == 0 && (rc = launch_region<true, CH>(L, b, work, part, width, ldw, n_chunks, epoch, st))) return rc;
   trsv_wide<true, CPL, PANEL><<<(int)grid, 32 * WW, dyn, st>>>(L, b, work, part, width, ldw, n_chunks, epoch);
-  int rc = check_launch("trsv_wide<fwd>");
+  rc = check_launch("trsv_wide<fwd>");
   if (rc) return rc;
+  if (l_reg && L.dense_r0 != 0 && (rc = launch_region<true, CH>(L, b, work, part, width, ldw, n_chunks, epoch, st))) return rc;
+  if (u_reg && U.dense_r0 == 0 && (rc = launch_region<false, CH>(U, x, work, part, width, ldw, n_chunks, epoch, st))) return rc;
   trsv_wide<false, CPL, PANEL><<<(int)grid, 32 * WW, dyn, st>>>(U, x, work, part, width, ldw, n_chunks, epoch);
-  return check_launch("trsv_wide<bwd>");
+  rc = check_launch("trsv_wide<bwd>");
+  if (rc) return rc;
+  if (u_reg && U.dense_r0 != 0) return launch_region<false, CH>(U, x, work, part, width, ldw, n_chunks, epoch, st);
+  return SGK_OK;
 }
 
 }  // namespace sgk

@@ -250,6 +250,7 @@ def _grouped(strict: csr_matrix, work_row, io_row, dinv):
         dense_g0=dg0, dense_nb=nb, dense_r0=dense[0], dense_pad=0, dense=bufs[14].data_ptr(),
     )
     st._host = (gptr, order, bufs[12], bufs[13])  # group structure + dense inverses for the wide form
+    st._dinv_host = None if dinv is None else np.asarray(dinv)
     return st, bufs, depth
 
 
@@ -446,6 +447,32 @@ def wide_panels(strict: csr_matrix, gptr: np.ndarray, order: np.ndarray, dense: 
                 pval=np.concatenate(pval) if pval else np.zeros(0), row_slot_ptr=rs_ptr, row_slot=rs)
 
 
+# explicit inverse of the dense region's triangle (one blocked product instead
+# of a chain of 32-row block solves) when its 1-norm condition estimate stays
+# below this bound; SGKKT_TRI_REGION_INV=0 disables it (A/B)
+REGION_INV = _os.environ.get("SGKKT_TRI_REGION_INV", "1") != "0"
+REGION_INV_MAX_COND = 1e10
+
+
+def region_inverse(strict: csr_matrix, dense: tuple[int, int], dinv) -> np.ndarray | None:
+    """inv(T), T = the dense region's triangle of `strict` with its diagonal
+    (unit for L, 1/dinv for the reversed U), or None when the region is empty,
+    neither leading nor trailing, or too ill-conditioned for an explicit
+    inverse (cond_1(T) > REGION_INV_MAX_COND: the blocks are streamed)."""
+    d0, d1 = dense
+    n = strict.shape[0]
+    if d1 <= d0 or not (d0 == 0 or d1 == n):
+        return None
+    m = d1 - d0
+    t = strict[d0:d1, d0:d1].toarray()
+    t[np.arange(m), np.arange(m)] = 1.0 if dinv is None else 1.0 / np.asarray(dinv)[d0:d1]
+    tinv = solve_triangular(t, np.eye(m), lower=True)
+    cond = np.abs(t).sum(axis=0).max() * np.abs(tinv).sum(axis=0).max()
+    if not np.isfinite(cond) or cond > REGION_INV_MAX_COND:
+        return None
+    return np.ascontiguousarray(np.tril(tinv))
+
+
 def _wide(strict: csr_matrix, grouped_bufs, st_grouped, work_row, io_row):
     """sgk_triwide for one processing-space triangle, sharing the grouped
     form's CSR, group pointer, row maps and dense inverses."""
@@ -477,8 +504,14 @@ def _wide(strict: csr_matrix, grouped_bufs, st_grouped, work_row, io_row):
         tile_kind=bufs[12].data_ptr(), dense_g0=g.dense_g0, dense_nb=g.dense_nb, dense_r0=g.dense_r0,
         dense_pad=0, dense=g.dense,
         pcol=extra[0].data_ptr() if panel else None, pval=extra[1].data_ptr() if panel else None,
-        tile_slot=extra[2].data_ptr() if panel else None,
+        tile_slot=extra[2].data_ptr() if panel else None, region_inv=None, part_rows=w["n_slots"], region_pad=0,
     )
+    if REGION_INV and g.dense_nb:
+        dinv_host = st_grouped._dinv_host
+        rinv = region_inverse(strict, dense, dinv_host)
+        if rinv is not None:
+            bufs.append(_f64(rinv.reshape(-1)))
+            st.region_inv = bufs[-1].data_ptr()
     return st, bufs, w["n_slots"]
 
 
@@ -612,7 +645,9 @@ class TriangularFactors:
             ldw = -(-width // ch) * ch
             dev = b_segs[0][0].device
             work = torch.empty((self.n, ldw), dtype=torch.float64, device=dev)
-            part = torch.empty((max(1, self.wl_slots, self.wu_slots), ldw), dtype=torch.float64, device=dev)
+            region_rows = DENSE_BLOCK * max(self.wl.dense_nb, self.wu.dense_nb)  # P rows of an inverted region
+            part = torch.empty((max(1, self.wl_slots, self.wu_slots) + region_rows, ldw), dtype=torch.float64,
+                               device=dev)
             if stream is not None:
                 work.record_stream(stream)
                 part.record_stream(stream)
