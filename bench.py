@@ -685,7 +685,8 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": (("stencil9_ws_kernel (warp-specialised: 8 producer + 8 consumer warps)"
+                     "kernel": (((("stencil9_tma_kernel (TMA/mbarrier pipeline" if os.environ.get("SGKKT_S9_TMA") != "0"
+                                   else "stencil9_ws_kernel (named barriers") + ": 8 producer + 8 consumer warps)")
                                  if 6 <= prog.host.stats.get("n_groups", 0) <= 8 and os.environ.get("SGKKT_S9_WS") != "0"
                                  else "stencil9_kernel")
                                 if prog.host.stats.get("mode") == "stencil9" else "program_kernel")

@@ -582,33 +582,61 @@ __global__ void region_prep(sgk_triwide t, sgk_segview io, const double* __restr
   }
 }
 
+// CTA = RT (64) region rows x CH columns, 256 threads of (64 / TY) rows x 4
+// columns each; 32-wide k tiles of inv(T) and P go through shared memory, the
+// next tile's global loads are issued before the current tile's products
+// (register prefetch), lower-triangular: k tiles up to the row tile's last row
+constexpr int RT = 64;
 template <bool FWD, int CH>
 __global__ void __launch_bounds__(256) region_gemm(sgk_triwide t, sgk_segview io, double* __restrict__ work,
                                                   const double* __restrict__ part, int width, int ldw, int n_chunks,
                                                   int epoch) {
-  constexpr int TX = CH / 4, TY = 256 / TX, RPT = WG / TY;  // thread: RPT rows x 4 columns
-  __shared__ double as[WG][WG + 1];
+  constexpr int TX = CH / 4, TY = 256 / TX, RPT = RT / TY;  // CH 64: 16 x 16 threads, 4 rows; CH 32: 8 x 32, 2 rows
+  constexpr int NA = RT * WG / 256, NP = WG * CH / 2 / 256;  // prefetch registers: doubles of A, double2 of P
+  __shared__ double as[RT][WG + 1];
   __shared__ __align__(16) double ps[WG][CH];
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
-  const int bi = t.dense_nb - 1 - blockIdx.x;  // longest products first
-  const int chunk = blockIdx.y, c0 = chunk * CH;
   const int m = WG * t.dense_nb;
+  const int n_rt = (m + RT - 1) / RT;
+  const int bi = n_rt - 1 - blockIdx.x;  // longest products first
+  const int chunk = blockIdx.y, c0 = chunk * CH;
+  const int row0 = RT * bi;
+  const int rows = min(RT, m - row0);
+  const int n_kb = (row0 + rows + WG - 1) / WG;
   const double* pd = part + (int64_t)t.part_rows * ldw + c0;
   double acc[RPT][4];
 #pragma unroll
   for (int j = 0; j < RPT; ++j)
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[j][c] = 0.0;
-  for (int kb = 0; kb <= bi; ++kb) {
-    for (int i = tid; i < WG * WG; i += 256) {
-      const int r = i / WG, k = i - r * WG;
-      as[r][k] = __ldg(t.region_inv + (int64_t)(WG * bi + r) * m + WG * kb + k);
+  double ra[NA];
+  double2 rp[NP];
+  auto fetch = [&](int kb) {
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      const int i = tid + 256 * u, r = i / WG, k = i - r * WG;
+      ra[u] = r < rows ? __ldg(t.region_inv + (int64_t)(row0 + r) * m + WG * kb + k) : 0.0;
     }
-    for (int i = tid; i < WG * CH / 2; i += 256) {
-      const int k = i / (CH / 2), c = 2 * (i - k * (CH / 2));
-      *reinterpret_cast<double2*>(&ps[k][c]) = __ldcg(reinterpret_cast<const double2*>(pd + (int64_t)(WG * kb + k) * ldw + c));
+#pragma unroll
+    for (int u = 0; u < NP; ++u) {
+      const int i = tid + 256 * u, k = i / (CH / 2), c = 2 * (i - k * (CH / 2));
+      rp[u] = __ldcg(reinterpret_cast<const double2*>(pd + (int64_t)(WG * kb + k) * ldw + c));
+    }
+  };
+  fetch(0);
+  for (int kb = 0; kb < n_kb; ++kb) {
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      const int i = tid + 256 * u, r = i / WG, k = i - r * WG;
+      as[r][k] = ra[u];
+    }
+#pragma unroll
+    for (int u = 0; u < NP; ++u) {
+      const int i = tid + 256 * u, k = i / (CH / 2), c = 2 * (i - k * (CH / 2));
+      *reinterpret_cast<double2*>(&ps[k][c]) = rp[u];
     }
     __syncthreads();
+    if (kb + 1 < n_kb) fetch(kb + 1);
 #pragma unroll 8
     for (int k = 0; k < WG; ++k) {
       const double2 p01 = *reinterpret_cast<const double2*>(&ps[k][4 * tx]);
@@ -626,33 +654,41 @@ __global__ void __launch_bounds__(256) region_gemm(sgk_triwide t, sgk_segview io
   }
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    const int p = t.dense_r0 + WG * bi + ty + TY * j;
-    double* wrow = work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + 4 * tx;
-    const int iorow = __ldg(t.io_row + p);
+    const int r = ty + TY * j;
+    if (r < rows) {
+      const int p = t.dense_r0 + row0 + r;
+      double* wrow = work + (int64_t)__ldg(t.work_row + p) * ldw + c0 + 4 * tx;
+      const int iorow = __ldg(t.io_row + p);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int col = c0 + 4 * tx + c;
-      __stcg(wrow + c, col < width ? acc[j][c] : 0.0);
-      if (!FWD && col < width) *wseg_ptr(io, iorow, col) = acc[j][c];
+      for (int c = 0; c < 4; ++c) {
+        const int col = c0 + 4 * tx + c;
+        __stcg(wrow + c, col < width ? acc[j][c] : 0.0);
+        if (!FWD && col < width) *wseg_ptr(io, iorow, col) = acc[j][c];
+      }
     }
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid < RT / WG && WG * tid < rows) {  // the row tile covers RT / WG region groups
     fence_acq_rel();
-    st_relaxed(t.flags + (int64_t)(t.dense_g0 + bi) * n_chunks + chunk, epoch);
+    st_relaxed(t.flags + (int64_t)(t.dense_g0 + (RT / WG) * bi + tid) * n_chunks + chunk, epoch);
   }
 }
 
 template <bool FWD, int CH>
 static int launch_region(const sgk_triwide& t, const sgk_segview& io, double* work, double* part, int width, int ldw,
                          int n_chunks, int epoch, cudaStream_t st) {
+  if constexpr (CH > 64) {  // 128-column chunks are not dispatched (sgk_trisolve_wide_chunk_cols)
+    set_error("region_gemm: chunk width above 64 columns");
+    return SGK_EINVAL;
+  } else {
   const int64_t total = (int64_t)WG * t.dense_nb * ldw;
   const int pgrid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 8);
   region_prep<FWD><<<pgrid, 256, 0, st>>>(t, io, work, part, width, ldw);
   int rc = check_launch("region_prep");
   if (rc) return rc;
-  region_gemm<FWD, CH><<<dim3(t.dense_nb, n_chunks), 256, 0, st>>>(t, io, work, part, width, ldw, n_chunks, epoch);
+  region_gemm<FWD, CH><<<dim3((WG * t.dense_nb + RT - 1) / RT, n_chunks), 256, 0, st>>>(t, io, work, part, width, ldw, n_chunks, epoch);
   return check_launch("region_gemm");
+  }
 }
 
 template <int CPL, bool PANEL>

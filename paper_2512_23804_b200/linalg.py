@@ -255,8 +255,8 @@ def _grouped(strict: csr_matrix, work_row, io_row, dinv):
 
 
 WIDE_SEG = 32     # entries per segment (one warp, <= 4 batches of 8 loads)
-WIDE_TILE_SEGS = 32
-WIDE_TILE_ENTRIES = 1024
+WIDE_TILE_SEGS = int(_os.environ.get("SGKKT_TRIW_TILE_SEGS", "32"))        # <= 32 (WSMAX in the kernel)
+WIDE_TILE_ENTRIES = int(_os.environ.get("SGKKT_TRIW_TILE_ENTRIES", "1024"))
 # SGKKT_TRI_WIDE_MIN: narrowest RHS width the wide-tiled solve takes (A/B)
 WIDE_MIN = int(__import__("os").environ.get("SGKKT_TRI_WIDE_MIN", "32"))
 
