@@ -685,7 +685,9 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": (((("stencil9_tma_kernel (TMA/mbarrier pipeline" if os.environ.get("SGKKT_S9_TMA") != "0"
+                     "kernel": (((("stencil9_grid_kernel<TMA> (grid form, sliding V window, TMA/mbarrier pipeline"
+                                   if os.environ.get("SGKKT_GRID9", "1") == "1" and os.environ.get("SGKKT_GRID_TMA") != "0"
+                                   else "stencil9_tma_kernel (TMA/mbarrier pipeline" if os.environ.get("SGKKT_S9_TMA") != "0"
                                    else "stencil9_ws_kernel (named barriers") + ": 8 producer + 8 consumer warps)")
                                  if 6 <= prog.host.stats.get("n_groups", 0) <= 8 and os.environ.get("SGKKT_S9_WS") != "0"
                                  else "stencil9_kernel")

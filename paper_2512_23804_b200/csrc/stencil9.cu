@@ -817,8 +817,11 @@ __global__ void __launch_bounds__((NPW + 8) * 32, 1) stencil9_tma_kernel(sgk_pat
                           (int)(((reinterpret_cast<uintptr_t>(pat.colind9) + (uintptr_t)row * 36) & 15) >> 2);
       if (rncols == kGroupCols) {  // common case: immediate column offsets
         const double* b = rvb + lane;
+#ifndef SGK_P_VN
+#define SGK_P_VN 9  // probe builds load fewer neighbour rows (sliding-window upper bound; results wrong)
+#endif
 #pragma unroll
-        for (int jj = 0; jj < 9; ++jj) {
+        for (int jj = 0; jj < SGK_P_VN; ++jj) {
           const double* vr = b + (int64_t)cg[jj] * rld;
 #pragma unroll
           for (int c = 0; c < kCols; ++c) v[c][jj] = SGK_VLD(vr + 32 * c);
@@ -986,7 +989,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
-template <int MAXOUT, bool ONEOUT>
+// TMA: the hand-over of stencil9_tma_kernel (bulk-copied coefficient ring issued by one consumer thread,
+// FULL/EMPTY mbarriers with one arrival per warp) instead of cp.async staging and named barriers
+// (measured and dropped: the next row's window column loaded straight into registers a product phase
+// ahead, with setmaxnreg 168 / 88 — 1.441 ms against 1.043 ms, gpurun_out/g59_ab.log)
+template <int MAXOUT, bool ONEOUT, int TMODE>
 __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk_program9 prog, ViewSet in,
                                                               ViewSet out, ViewSet init, ScalarSet alpha,
                                                               ScalarSet beta) {
@@ -1001,6 +1008,10 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
   int32_t* coff = reinterpret_cast<int32_t*>(sm + L.coff);
   uint32_t* gent = reinterpret_cast<uint32_t*>(sm + L.gent);
   const int ustride = (int)(align16(sizeof(double) * ((size_t)prog.n_ubuf + 64)));
+  constexpr bool TMA = TMODE != 0;
+  unsigned char* ring = sm + L.total;  // TMA: kRing slots of the row's coefficient block
+  const int slot_bytes = (int)align16(sizeof(double) * 10 * (size_t)gp.n_slices);
+  __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2], bar_coef[kRing];
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -1013,6 +1024,14 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
     const sgk_view& vv = pick(in, tid);
     in_ptr[tid] = vv.ptr + vv.col0;
     in_ld[tid] = vv.ld;
+  }
+  if (TMA && tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_full[b], 8);
+      mbar_init(&bar_empty[b], 8);
+    }
+    for (int b = 0; b < kRing; ++b) mbar_init(&bar_coef[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int ncoef = gp.n_slices * 10;
   for (int i = tid; i < prog.n_coef; i += blockDim.x) ctab[i] = prog.coef_tab[i];
@@ -1180,7 +1199,7 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
     int sg = s_first + blockIdx.x, node = 0, nend = 0;
     bool have = sg <= s_last;
     if (have) seg_range(sg, node, nend);
-    if (have) stage(node - A, 0);
+    if (!TMA && have) stage(node - A, 0);
     cp_async_commit();
     if (active && have) window_unified(node, true);
     int it = 0;
@@ -1189,6 +1208,18 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
       int sg_n = sg, node_n = node, nend_n = nend;
       bool restart_n = false;
       const bool have_n = advance(sg_n, node_n, nend_n, restart_n);
+      if constexpr (TMA) {
+        if (active) {
+          // the window registers are in (the last staged column's LDS have returned) before the
+          // staging slots are overwritten
+          const double chk = rv[0][2] + rv[kCols - 1][5] + rv[kCols - 1][8];
+          if (chk == 1.2345e-300) ubuf[prog.n_ubuf] = chk;
+          if (have_n && !restart_n) stage_v(node_n, 1);  // a whole product phase ahead of its use
+          cp_async_commit();
+          mbar_wait(&bar_coef[it & (kRing - 1)], (it >> 2) & 1);
+        }
+        if (it >= 2) mbar_wait(&bar_empty[cb], ((it >> 1) & 1) ^ 1);  // consumers are done with U buffer cb
+      } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       bar_sync_n(5, 256);  // this row's coefficients visible; every producer is done with row it-1
       if (have_n) stage(node_n - A, cb ^ 1);
@@ -1197,8 +1228,10 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
       if (active && have_n && !restart_n) stage_v(node_n, 1);
       cp_async_commit();
       if (it >= 2) bar_sync_n(3 + cb, 512);  // consumers are done with U buffer cb (row it-2)
+      }
       if (active) {
-        const double* crow = coef_s + cb * ncoef;
+        const double* crow = TMA ? reinterpret_cast<const double*>(ring + (it & (kRing - 1)) * slot_bytes)
+                                 : coef_s + cb * ncoef;
         double* ubq = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ubuf) + cb * ustride) + rbase;
         int recn = rq0 < rq1 ? steps[rq0] : 0;
         double2 p01 = make_double2(0.0, 0.0), p23 = p01;
@@ -1231,17 +1264,37 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
           for (int c = 0; c < kCols; ++c) ub[32 * c] = dot9(a, rv[c]);
         }
       }
-      bar_arrive_n(1 + cb, 512);  // U buffer cb holds row it
+      if constexpr (TMA) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_full[cb]);
+      } else {
+        bar_arrive_n(1 + cb, 512);  // U buffer cb holds row it
+      }
       if (active && have_n) window_unified(node_n, restart_n);  // next row's window
       sg = sg_n;
       node = node_n;
       nend = nend_n;
       have = have_n;
     }
-    for (int k = (it >= 2 ? it - 2 : 0); k < it; ++k) bar_sync_n(3 + (k & 1), 512);
+    if constexpr (!TMA)
+      for (int k = (it >= 2 ? it - 2 : 0); k < it; ++k) bar_sync_n(3 + (k & 1), 512);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else {
     const int cw = warp - 8;
+    // TMA: thread 256 runs kRing rows ahead of the consumers and bulk-copies each row's coefficient block
+    int isg = s_first + blockIdx.x, inode = 0, inend = 0, iit = 0;
+    bool ihave = TMA && tid == 256 && isg <= s_last;
+    auto issue_next = [&]() {
+      uint64_t* bar = &bar_coef[iit & (kRing - 1)];
+      mbar_expect_tx(bar, (uint32_t)(ncoef * sizeof(double)));
+      bulk_load(ring + (iit & (kRing - 1)) * slot_bytes, gp.coefg + (int64_t)inode * ncoef,
+                (uint32_t)(ncoef * sizeof(double)), bar);
+      ++iit;
+      bool r;
+      ihave = advance(isg, inode, inend, r);
+    };
+    if (ihave) seg_range(isg, inode, inend);
+    for (int q = 0; q < kRing && ihave; ++q) issue_next();
     int ocol[MAXOUT];
 #pragma unroll
     for (int r = 0; r < MAXOUT; ++r) {
@@ -1254,7 +1307,12 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
     for (int it = 0; have; ++it) {
       const int row = node - A;  // local output row
       const int cb = it & 1;
-      bar_sync_n(1 + cb, 512);  // products of this row are in U buffer cb
+      if constexpr (TMA) {
+        mbar_wait(&bar_full[cb], (it >> 1) & 1);  // products of this row are in U buffer cb
+        if (ihave) issue_next();  // every producer is past row it: its ring slot is free
+      } else {
+        bar_sync_n(1 + cb, 512);  // products of this row are in U buffer cb
+      }
       const unsigned char* smb = sm + cb * ustride;
       double* orow = nullptr;
       const double* irow = nullptr;
@@ -1300,39 +1358,60 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
           }
         }
       }
-      bar_arrive_n(3 + cb, 512);  // done reading U buffer cb
+      if constexpr (TMA) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_empty[cb]);
+      } else {
+        bar_arrive_n(3 + cb, 512);  // done reading U buffer cb
+      }
       bool restart;
       have = advance(sg, node, nend, restart);
     }
   }
 }
 
-template <int MAXOUT, bool ONEOUT>
-static int launch9grid(const sgk_grid9& gp, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
+template <int MAXOUT, bool ONEOUT, int TMA>
+static int launch9grid_t(const sgk_grid9& gp, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
                        const ViewSet& init, const ScalarSet& a, const ScalarSet& b, cudaStream_t st) {
   const Smem9 L = smem9_grid_layout(gp.n_slices, prog);
+  const size_t total = L.total + (TMA ? kRing * align16(sizeof(double) * 10 * (size_t)gp.n_slices) : 0);
   static bool attr_set = false;
   if (!attr_set) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, stencil9_grid_kernel<MAXOUT, ONEOUT>);
-    cudaFuncSetAttribute(stencil9_grid_kernel<MAXOUT, ONEOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncGetAttributes(&fa, stencil9_grid_kernel<MAXOUT, ONEOUT, TMA>);
+    cudaFuncSetAttribute(stencil9_grid_kernel<MAXOUT, ONEOUT, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          optin - (int)fa.sharedSizeBytes);
     cudaGetLastError();
     attr_set = true;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_grid_kernel<MAXOUT, ONEOUT>, 512, L.total);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil9_grid_kernel<MAXOUT, ONEOUT, TMA>, 512, total);
   if (occ < 1) {
-    set_error("stencil9_grid_kernel: program does not fit in shared memory (" + std::to_string(L.total) + " B)");
+    set_error("stencil9_grid_kernel: program does not fit in shared memory (" + std::to_string(total) + " B)");
     return SGK_ELIMIT;
   }
   int64_t grid = (int64_t)sm_count() * occ;
   if (grid < 1) return SGK_OK;
-  stencil9_grid_kernel<MAXOUT, ONEOUT><<<(int)grid, 512, L.total, st>>>(gp, prog, in, out, init, a, b);
+  stencil9_grid_kernel<MAXOUT, ONEOUT, TMA><<<(int)grid, 512, total, st>>>(gp, prog, in, out, init, a, b);
   return check_launch("stencil9_grid_kernel");
+}
+
+// SGKKT_GRID_TMA=0: the named-barrier hand-over of the grid kernel (A/B)
+template <int MAXOUT, bool ONEOUT>
+static int launch9grid(const sgk_grid9& gp, const sgk_program9& prog, const ViewSet& in, const ViewSet& out,
+                       const ViewSet& init, const ScalarSet& a, const ScalarSet& b, cudaStream_t st) {
+  static const int tma_env = [] {
+    const char* v = getenv("SGKKT_GRID_TMA");
+    return v ? atoi(v) : 1;
+  }();
+  if (tma_env) {
+    const int rc = launch9grid_t<MAXOUT, ONEOUT, 1>(gp, prog, in, out, init, a, b, st);
+    if (rc != SGK_ELIMIT) return rc;
+  }
+  return launch9grid_t<MAXOUT, ONEOUT, 0>(gp, prog, in, out, init, a, b, st);
 }
 
 template <int MAXOUT, bool ONEOUT>

@@ -28,11 +28,13 @@ F64 = torch.float64
 import os as _os
 
 FAST9 = _os.environ.get("SGKKT_FAST9", "1") != "0"
-# SGKKT_GRID9=1 runs the config-4 matvec on the grid-form WS kernel (sliding
-# V window, grid-line segment walk): bit-identical, 30 % fewer L1 wavefronts,
-# but measured 1.126 ms vs 1.100 ms for the pattern-indexed WS kernel
-# (profiles/r02_grid_ab.txt) — off by default, kept for A/B
-GRID9 = _os.environ.get("SGKKT_GRID9", "0") == "1"
+# Product-heavy single-input programs on a Q1 grid pattern (the config-4
+# matvec) run the grid-form kernel: sliding V window along grid-line segments
+# (3 new neighbour rows per mesh row instead of 9), bit-identical.  With the
+# round-1 named-barrier hand-over it measured 1.141 ms against 1.092 ms for
+# the pattern-indexed kernel; on the TMA/mbarrier pipeline 1.043 ms against
+# 1.070 ms (gpurun_out/g56_ab.log) — on by default, SGKKT_GRID9=0 for A/B
+GRID9 = _os.environ.get("SGKKT_GRID9", "1") == "1"
 # output columns one launch can hold (16 gather chunks x 256 threads in both
 # kernels); wider programs are launched per column block
 MAX_LAUNCH_COLS = 16 * 256
