@@ -144,6 +144,9 @@ typedef struct {
   const int32_t* gather_ptr; /* [2*n_chunks]                                */
   const uint32_t* gather_ent;/* [n_gather]                                  */
   const int32_t* out_col;    /* [32*n_chunks]                               */
+  double coef8[8];           /* host copy of coef_tab[0..8) (n_coef <= 8: the
+                              * grid kernel's gather reads the coefficients from
+                              * the kernel parameter bank, not shared memory) */
 } sgk_program9;
 
 /* Same contract as sgk_program_apply for a padded 9-point pattern.  Returns

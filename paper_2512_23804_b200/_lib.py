@@ -86,6 +86,7 @@ class Program9(ctypes.Structure):
         ("n_coef", c_i32), ("n_gather", c_i32), ("n_slices", c_i32), ("n_chunks", c_i32), ("group_info", c_vp),
         ("step_rec", c_vp),
         ("coef_tab", c_vp), ("gather_ptr", c_vp), ("gather_ent", c_vp), ("out_col", c_vp),
+        ("coef8", c_dbl * 8),
     ]
 
 

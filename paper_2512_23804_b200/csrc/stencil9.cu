@@ -91,7 +91,7 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // BIG: 9..16 column groups, one CTA of up to 16 warps per SM so every group
 // stays resident (V prefetched) instead of warps looping over two groups
 template <int MAXOUT, bool RESIDENT, bool ONEOUT, bool BIG>
-__global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stencil9_kernel(sgk_pattern9 pat, sgk_program9 prog, ViewSet in,
+__global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stencil9_kernel(sgk_pattern9 pat, const __grid_constant__ sgk_program9 prog, ViewSet in,
                                                           ViewSet out, ViewSet init, ScalarSet alpha,
                                                           ScalarSet beta) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -353,6 +353,16 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
       const int npair = ccnt[chunk] >> 1;
       const uint2* gp = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
       double acc0 = 0.0, acc1 = 0.0;
+#ifdef SGK_ALT_COEF_LDC
+      if (prog.n_coef <= 8) {  // coefficients from the kernel parameter bank (see stencil9_grid_kernel)
+#pragma unroll 2
+        for (int e = 0; e < npair; ++e, gp += 32) {
+          const uint2 w = *gp;
+          acc0 = fma(prog.coef8[(w.x >> 3) & 7], *reinterpret_cast<const double*>(sm + (w.x >> 14)), acc0);
+          acc1 = fma(prog.coef8[(w.y >> 3) & 7], *reinterpret_cast<const double*>(sm + (w.y >> 14)), acc1);
+        }
+      } else
+#endif
 #pragma unroll 2
       for (int e = 0; e < npair; ++e, gp += 32) {
         const uint2 w = *gp;
@@ -694,12 +704,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "{\n"
       ".reg .pred P1;\n"
       "LAB_WAIT:\n"
+#ifdef SGK_MBAR_HINT
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+#else
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+#endif
       "@P1 bra DONE;\n"
       "bra LAB_WAIT;\n"
       "DONE:\n"
       "}" ::"r"(smem_u32(b)),
       "r"(parity)
+#ifdef SGK_MBAR_HINT
+      , "r"(SGK_MBAR_HINT)
+#endif
       : "memory");
 }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
@@ -994,7 +1011,7 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 // (measured and dropped: the next row's window column loaded straight into registers a product phase
 // ahead, with setmaxnreg 168 / 88 — 1.441 ms against 1.043 ms, gpurun_out/g59_ab.log)
 template <int MAXOUT, bool ONEOUT, int TMODE>
-__global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk_program9 prog, ViewSet in,
+__global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, const __grid_constant__ sgk_program9 prog, ViewSet in,
                                                               ViewSet out, ViewSet init, ScalarSet alpha,
                                                               ScalarSet beta) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -1296,11 +1313,19 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
     if (ihave) seg_range(isg, inode, inend);
     for (int q = 0; q < kRing && ihave; ++q) issue_next();
     int ocol[MAXOUT];
+    // row-invariant gather bookkeeping of this warp's chunks, kept in registers
+    // (a shared-memory read per chunk and row sat in front of every entry load)
+    int npair_r[MAXOUT];
+    const uint2* gpe_r[MAXOUT];
 #pragma unroll
     for (int r = 0; r < MAXOUT; ++r) {
       const int chunk = cw + r * 8;
       ocol[r] = chunk < n_chunks ? __ldg(prog.out_col + chunk * 32 + lane) : -1;
+      npair_r[r] = chunk < n_chunks ? ccnt[chunk] >> 1 : 0;
+      gpe_r[r] = reinterpret_cast<const uint2*>(gent + (chunk < n_chunks ? coff[chunk] : 0)) + lane;
     }
+    // (measured and dropped: the first 1..4 entry pairs of every chunk in registers, so their U loads
+    // issue with no entry load in front: 0.995 / 1.024 / 1.014 / 1.017 ms against 0.990, g63/g64_ab.log)
     int sg = s_first + blockIdx.x, node = 0, nend = 0;
     bool have = sg <= s_last;
     if (have) seg_range(sg, node, nend);
@@ -1324,9 +1349,21 @@ __global__ void __launch_bounds__(512, 1) stencil9_grid_kernel(sgk_grid9 gp, sgk
       for (int rb = 0; rb < MAXOUT; ++rb) {
         const int chunk = cw + rb * 8;
         if (chunk >= n_chunks) break;
-        const int npair = SGK_DBG_NPAIR;
-        const uint2* gpe = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
+        const int npair = npair_r[rb];
+        const uint2* gpe = gpe_r[rb];
         double acc0 = 0.0, acc1 = 0.0;
+#ifndef SGK_NO_COEF_LDC
+        if (TMA && prog.n_coef <= 8) {
+          // <= 8 distinct coefficients: read from the kernel parameter bank (constant
+          // cache, its own pipe) by index instead of from shared memory (1.044 -> 1.019 ms; unrolled 4x: 1.008)
+#pragma unroll 4
+          for (int e = 0; e < npair; ++e, gpe += 32) {
+            const uint2 w = *gpe;
+            acc0 = fma(prog.coef8[(w.x >> 3) & 7], *reinterpret_cast<const double*>(smb + (w.x >> 14)), acc0);
+            acc1 = fma(prog.coef8[(w.y >> 3) & 7], *reinterpret_cast<const double*>(smb + (w.y >> 14)), acc1);
+          }
+        } else
+#endif
 #pragma unroll 2
         for (int e = 0; e < npair; ++e, gpe += 32) {
           const uint2 w = *gpe;

@@ -311,6 +311,7 @@ class _Program9:
             group_info=b[0].data_ptr(), step_rec=b[1].data_ptr(),
             coef_tab=b[2].data_ptr(), gather_ptr=b[3].data_ptr(), gather_ent=b[4].data_ptr(),
             out_col=b[5].data_ptr(),
+            coef8=(ctypes.c_double * 8)(*[float(v) for v in np.asarray(host.coef_tab, np.float64).reshape(-1)[:8]]),
         )
 
 
