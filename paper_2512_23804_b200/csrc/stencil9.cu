@@ -31,6 +31,10 @@ constexpr int kGroupCols = 32 * kCols;  // columns of one group (one warp)
 #ifndef SGK_VLD
 #define SGK_VLD __ldg
 #endif
+#ifndef SGK_ALT_LDC_UNROLL
+#define SGK_ALT_LDC_UNROLL 2
+#endif
+constexpr int kAltLdcUnroll = SGK_ALT_LDC_UNROLL;  // gather unroll of stencil9_kernel's parameter-bank path
 
 // Shared-memory map.  ubuf holds n_ubuf U slots + 32 trash slots (inactive
 // (step, column-slot) pairs store there) + 32 zero slots (gather padding).
@@ -353,9 +357,10 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
       const int npair = ccnt[chunk] >> 1;
       const uint2* gp = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
       double acc0 = 0.0, acc1 = 0.0;
-#ifdef SGK_ALT_COEF_LDC
-      if (prog.n_coef <= 8) {  // coefficients from the kernel parameter bank (see stencil9_grid_kernel)
-#pragma unroll 2
+#ifndef SGK_NO_COEF_LDC
+      if (prog.n_coef <= 8) {  // coefficients from the kernel parameter bank (see stencil9_grid_kernel;
+                               // config-5 KKT matvec 0.455 -> 0.434 ms)
+#pragma unroll kAltLdcUnroll
         for (int e = 0; e < npair; ++e, gp += 32) {
           const uint2 w = *gp;
           acc0 = fma(prog.coef8[(w.x >> 3) & 7], *reinterpret_cast<const double*>(sm + (w.x >> 14)), acc0);
