@@ -704,6 +704,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
+#define SGK_STR2(x) #x
+#define SGK_STR(x) SGK_STR2(x)
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -715,6 +717,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
 #endif
       "@P1 bra DONE;\n"
+#ifdef SGK_MBAR_SLEEP
+      "nanosleep.u32 " SGK_STR(SGK_MBAR_SLEEP) ";\n"
+#endif
       "bra LAB_WAIT;\n"
       "DONE:\n"
       "}" ::"r"(smem_u32(b)),
