@@ -137,10 +137,17 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
   for (int i = tid; i < 64; i += blockDim.x) ubuf[prog.n_ubuf + i] = 0.0;
 
   int ocol[MAXOUT];
+  // a chunk never spans two outputs (program.py: positions are padded to whole
+  // chunks per output), so the output index of a chunk is warp-uniform: two
+  // bits per chunk, found once; the multi-output epilogue then branches on it
+  // and reads the views straight from the parameter bank instead of running
+  // select chains per element
+  uint32_t opack = 0;
 #pragma unroll
   for (int r = 0; r < MAXOUT; ++r) {
     const int chunk = warp + r * nwarps;
     ocol[r] = chunk < n_chunks ? __ldg(prog.out_col + chunk * 32 + lane) : -1;
+    if constexpr (!ONEOUT) opack |= (uint32_t)max(__reduce_max_sync(0xffffffffu, ocol[r] >> 24), 0) << (2 * r);
   }
 
   auto stage = [&](int row, int buf) {
@@ -387,18 +394,18 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
           // per-lane output index: select the view fields by value (a
           // reference into the parameter views with a per-lane index makes
           // the compiler copy them to local memory on every output)
-          const int o = oc >> 24, k = oc & 0xFFFFFF;
-          const double al = sel4(alpha.s[0], alpha.s[1], alpha.s[2], alpha.s[3], o);
-          const double be = sel4(beta.s[0], beta.s[1], beta.s[2], beta.s[3], o);
-          const double* ip = sel4(init.v[0].ptr, init.v[1].ptr, init.v[2].ptr, init.v[3].ptr, o);
-          const int64_t il = sel4(init.v[0].ld, init.v[1].ld, init.v[2].ld, init.v[3].ld, o);
-          const int ic = sel4(init.v[0].col0, init.v[1].col0, init.v[2].col0, init.v[3].col0, o);
-          double* op = sel4(out.v[0].ptr, out.v[1].ptr, out.v[2].ptr, out.v[3].ptr, o);
-          const int64_t ol = sel4(out.v[0].ld, out.v[1].ld, out.v[2].ld, out.v[3].ld, o);
-          const int occ = sel4(out.v[0].col0, out.v[1].col0, out.v[2].col0, out.v[3].col0, o);
-          double y = al * acc;
-          if (ip != nullptr) y += be * ip[(int64_t)row * il + ic + k];
-          op[(int64_t)row * ol + occ + k] = y;
+          const int k = oc & 0xFFFFFF;
+          auto emit = [&](const sgk_view& ov, const sgk_view& iv, double al, double be) {
+            double y = al * acc;
+            if (iv.ptr != nullptr) y += be * iv.ptr[(int64_t)row * iv.ld + iv.col0 + k];
+            ov.ptr[(int64_t)row * ov.ld + ov.col0 + k] = y;
+          };
+          switch ((opack >> (2 * rb)) & 3u) {  // warp-uniform
+            case 0: emit(out.v[0], init.v[0], alpha.s[0], beta.s[0]); break;
+            case 1: emit(out.v[1], init.v[1], alpha.s[1], beta.s[1]); break;
+            case 2: emit(out.v[2], init.v[2], alpha.s[2], beta.s[2]); break;
+            default: emit(out.v[3], init.v[3], alpha.s[3], beta.s[3]); break;
+          }
         }
       }
     }
