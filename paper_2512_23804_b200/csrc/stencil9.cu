@@ -158,6 +158,19 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
   };
 
   __syncthreads();  // tables and input views visible
+  // row-invariant gather bookkeeping of this warp's chunks in registers (as in
+  // stencil9_grid_kernel) when the warp has at most four chunks
+  constexpr bool kHoist = MAXOUT <= 4;
+  int npair_r[kHoist ? MAXOUT : 1];
+  const uint2* gp_r[kHoist ? MAXOUT : 1];
+  if constexpr (kHoist) {
+#pragma unroll
+    for (int r = 0; r < MAXOUT; ++r) {
+      const int chunk = warp + r * nwarps;
+      npair_r[r] = chunk < n_chunks ? ccnt[chunk] >> 1 : 0;
+      gp_r[r] = reinterpret_cast<const uint2*>(gent + (chunk < n_chunks ? coff[chunk] : 0)) + lane;
+    }
+  }
 
   // resident mode: every warp owns at most one group for the whole kernel, so
   // its 36 V values of the next row can be prefetched during the gather phase
@@ -361,8 +374,8 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : SGK_S9_MINB) stenci
     for (int rb = 0; rb < MAXOUT; ++rb) {
       const int chunk = warp + rb * nwarps;
       if (chunk >= n_chunks) break;
-      const int npair = ccnt[chunk] >> 1;
-      const uint2* gp = reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
+      const int npair = kHoist ? npair_r[kHoist ? rb : 0] : ccnt[chunk] >> 1;
+      const uint2* gp = kHoist ? gp_r[kHoist ? rb : 0] : reinterpret_cast<const uint2*>(gent + coff[chunk]) + lane;
       double acc0 = 0.0, acc1 = 0.0;
 #ifndef SGK_NO_COEF_LDC
       if (prog.n_coef <= 8) {  // coefficients from the kernel parameter bank (see stencil9_grid_kernel;
